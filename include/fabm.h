@@ -1,0 +1,176 @@
+/*
+ * fabm.h — C ABI of the B200-native fractional Adams–Bashforth–Moulton (ABM)
+ * history engine (libfabm.so).
+ *
+ * The reference package `fodeabm` has no FFI: its drop-in boundary is the
+ * Python solver call
+ *
+ *     solve_serial(problem: FractionalProblem, grid: GridSpec) -> Trajectory
+ *         (/root/reference/pkg/src/fodeabm/serial.py:114-176)
+ *
+ * plus the strategy dispatch strings (bench.py:43-51, cli.py:86-94) and the
+ * weight seam `precompute_weights` (core.py:134-154, serial.py:130).  Every
+ * entry point below replaces one of those; the replaced interface is cited
+ * next to each declaration.  Signatures use plain C types only (no torch,
+ * no CUDA types): pointers are HOST pointers unless the name says `_device`.
+ *
+ * Conventions carried over from the reference:
+ *   - errors: a bad configuration returns FABM_ERR_CONFIG (the reference's
+ *     ValueError, core.py:62-66,203-220; serial.py:125-129); a non-finite
+ *     rhs output returns FABM_ERR_NONFINITE with the loop index `step` and
+ *     t = (step+1)*h of the first failing evaluation (SolverStepError,
+ *     core.py:34-43, serial.py:157-174); a stuck solve returns
+ *     FABM_ERR_TIMEOUT (StrategyTimeoutError, core.py:46-47).
+ *   - calls are synchronous: they return when the whole trajectory is done
+ *     (SPEC.md:128); outputs are fresh caller-owned buffers.
+ *   - determinism: identical inputs give bitwise identical outputs
+ *     (bench.py:80-87 enforces this for every strategy).
+ */
+#ifndef FABM_H
+#define FABM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FABM_MAX_DIM 4      /* state dimension supported by the device engine */
+#define FABM_MAX_PARAMS 16  /* rhs parameters per problem */
+
+/* status codes */
+enum {
+  FABM_OK = 0,
+  FABM_ERR_NONFINITE = 1, /* SolverStepError: rhs returned a non-finite value */
+  FABM_ERR_CONFIG = 2,    /* ValueError: bad alpha/dim/y0/grid/system */
+  FABM_ERR_TIMEOUT = 3,   /* StrategyTimeoutError: device watchdog expired */
+  FABM_ERR_CUDA = 4,      /* CUDA runtime failure (message in status) */
+  FABM_ERR_NODEVICE = 5   /* no usable sm_100 device */
+};
+
+/* which rhs evaluation failed (fabm_status.kind) */
+enum {
+  FABM_KIND_NONE = 0,
+  FABM_KIND_INITIAL = 1,   /* f(0, y0)          core.py:226-236            */
+  FABM_KIND_PREDICTOR = 2, /* f(t_{n+1}, yP)    serial.py:156-158          */
+  FABM_KIND_CORRECTOR = 3  /* f(t_{n+1}, y_{n+1}) serial.py:166-168        */
+};
+
+/* device right-hand sides (systems.py:26-123 + the BASELINE.json systems) */
+enum {
+  FABM_SYS_CONSTANT = 0,       /* params[0..d-1] = value            systems.py:26-36  */
+  FABM_SYS_POWER_LAW = 1,      /* params = {coef, expo}             systems.py:39-61  */
+  FABM_SYS_LINEAR = 2,         /* params = {lam}                    systems.py:64-73  */
+  FABM_SYS_HINDMARSH_ROSE = 3, /* params = {a,b,c,d,r,s,x_rest,i}   systems.py:101-123 */
+  FABM_SYS_LORENZ = 4,         /* params = {sigma, rho, beta}                         */
+  FABM_SYS_CHEN = 5,           /* params = {a, b, c}                                  */
+  FABM_SYS_ROSSLER = 6,        /* params = {a, b, c}                                  */
+  FABM_SYS_FINANCIAL = 7       /* params = {a, b, c}                                  */
+};
+
+/* weight generation modes (fabm_weights / fabm_plan_set_weights) */
+enum {
+  FABM_WEIGHTS_ACCURATE = 0, /* device, cancellation-free series (few ulp)          */
+  FABM_WEIGHTS_FORMULA = 1,  /* device, the reference's pow formula (core.py:149-151) */
+  FABM_WEIGHTS_HOST = 2      /* caller-provided table (the precompute_weights seam) */
+};
+
+/* FractionalProblem (core.py:188-236) with a device rhs tag instead of a
+ * Python callable. */
+typedef struct fabm_problem {
+  double alpha;                     /* (0, 1]                                  */
+  int32_t dim;                      /* 1..FABM_MAX_DIM                         */
+  int32_t system;                   /* FABM_SYS_*                              */
+  double params[FABM_MAX_PARAMS];
+  double y0[FABM_MAX_DIM];
+} fabm_problem;
+
+/* GridSpec (core.py:157-185) plus the per-solve scalars serial.py:135-136
+ * computes in Python.  The caller passes them so the device uses the very
+ * same bits (CPython's math.gamma is not libm's tgamma).  A zero field is
+ * filled by the library from libm. */
+typedef struct fabm_grid {
+  int64_t n_steps;   /* N >= 1                                       */
+  double h;          /* step size                                    */
+  double h_alpha;    /* h ** alpha                  (serial.py:135)  */
+  double inv_gamma2; /* 1 / Gamma(alpha + 2)        (serial.py:136)  */
+  double gamma1;     /* Gamma(alpha + 1)            (core.py:146)    */
+  double gamma2;     /* Gamma(alpha + 2)            (core.py:147)    */
+} fabm_grid;
+
+typedef struct fabm_status {
+  int32_t code;      /* FABM_OK / FABM_ERR_*                         */
+  int32_t kind;      /* FABM_KIND_* for FABM_ERR_NONFINITE           */
+  int64_t step;      /* loop index n of the failing step             */
+  double t;          /* (n + 1) * h                                  */
+  char message[240];
+} fabm_status;
+
+typedef struct fabm_stats {
+  double kernel_ms;        /* engine kernel, CUDA events on the engine stream   */
+  double weights_ms;       /* weight-generation kernel                          */
+  int64_t steps;           /* steps taken                                       */
+  int64_t history_fma;     /* algorithmic history FMAs per trajectory = d*N^2   */
+  int64_t bulk_tiles;      /* Toeplitz tiles processed by the bulk agents       */
+  int64_t leader_wait_ns;  /* time the stepper spent waiting on handoffs        */
+  int32_t bulk_ctas;       /* CTAs running bulk agents                          */
+  int32_t block;           /* history block B                                   */
+  int32_t window_blocks;   /* stepper window L (blocks)                         */
+  int32_t reserved;
+} fabm_stats;
+
+typedef struct fabm_plan fabm_plan;
+
+/* ---- library ---------------------------------------------------------- */
+const char* fabm_version(void);
+int fabm_device_count(void);
+
+/* ---- weights: replaces precompute_weights (core.py:134-154) -----------
+ * Fills b, a, c (host buffers of n_steps+1 doubles) using the device
+ * generator in `mode` (FABM_WEIGHTS_ACCURATE or FABM_WEIGHTS_FORMULA). */
+int fabm_weights(double alpha, int64_t n_steps, int mode, double gamma1,
+                 double gamma2, double* b, double* a, double* c,
+                 fabm_status* status);
+
+/* ---- one trajectory: replaces solve_serial (serial.py:114-176) ---------
+ * states and f_cache are host buffers of (n_steps+1)*dim doubles, row n =
+ * y_n / f(t_n, y_n) (Trajectory, serial.py:36-64).  When weight_mode is
+ * FABM_WEIGHTS_HOST, b/a/c point at n_steps+1 doubles each (the table the
+ * reference's precompute_weights returned); otherwise they may be NULL. */
+int fabm_solve(const fabm_problem* problem, const fabm_grid* grid,
+               int weight_mode, const double* b, const double* a,
+               const double* c, double* states, double* f_cache,
+               fabm_status* status);
+
+/* ---- plan API: device-resident buffers, for repeated solves/benchmarks - */
+fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid,
+                            int device, fabm_status* status);
+int fabm_plan_set_weights(fabm_plan* plan, int weight_mode, const double* b,
+                          const double* a, const double* c, fabm_status* status);
+/* upload y0 (host) for this run; NULL keeps the plan's current y0 */
+int fabm_plan_set_y0(fabm_plan* plan, const double* y0, fabm_status* status);
+/* run the engine on the plan's stream; inputs must already be resident */
+int fabm_plan_run(fabm_plan* plan, double timeout_s, fabm_status* status);
+int fabm_plan_download(fabm_plan* plan, double* states, double* f_cache,
+                       fabm_status* status);
+/* final state y_N only (d doubles) — the small D2H read of the bench */
+int fabm_plan_download_last(fabm_plan* plan, double* y_last, fabm_status* status);
+int fabm_plan_stats(const fabm_plan* plan, fabm_stats* stats);
+void fabm_plan_destroy(fabm_plan* plan);
+
+/* ---- batch: many independent trajectories (BASELINE config 4) ----------
+ * problems[count], grids[count] share n_steps and h; states/f_cache (may be
+ * NULL for f_cache) hold count*(n_steps+1)*dim doubles, trajectory-major.
+ * Weights are generated on device per trajectory (alpha differs). */
+int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids,
+                     int64_t count, int device, double* states,
+                     double* f_cache, double* kernel_ms, fabm_status* status);
+
+/* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
+/* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */
+double fabm_measure_dfma_peak(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FABM_H */

@@ -1,0 +1,510 @@
+// fabm_api.cu — the C ABI declared in include/fabm.h (libfabm.so).
+//
+// Host-side runtime: device buffers per plan (one stream, CUDA events for
+// timing), weight generation, cooperative launch of the history engine,
+// status translation.  No torch types cross this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/fabm.h"
+#include "engine.cuh"
+#include "weights.cuh"
+
+using namespace fabm;
+
+namespace {
+
+constexpr const char* kVersion = "fabm-b200 0.1.0 (sm_100a)";
+
+void set_status(fabm_status* st, int code, const char* fmt, ...) {
+  if (!st) return;
+  st->code = code;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(st->message, sizeof(st->message), fmt, ap);
+  va_end(ap);
+}
+
+void clear_status(fabm_status* st) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      set_status(status, FABM_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e));   \
+      return FABM_ERR_CUDA;                                                         \
+    }                                                                               \
+  } while (0)
+
+bool system_dim_ok(int sys, int dim) {
+  switch (sys) {
+    case FABM_SYS_CONSTANT:
+    case FABM_SYS_LINEAR: return dim >= 1 && dim <= FABM_MAX_DIM;
+    case FABM_SYS_POWER_LAW: return dim == 1;
+    case FABM_SYS_HINDMARSH_ROSE:
+    case FABM_SYS_LORENZ:
+    case FABM_SYS_CHEN:
+    case FABM_SYS_ROSSLER:
+    case FABM_SYS_FINANCIAL: return dim == 3;
+    default: return false;
+  }
+}
+
+int validate(const fabm_problem* p, const fabm_grid* g, fabm_status* status) {
+  if (!p || !g) { set_status(status, FABM_ERR_CONFIG, "null problem or grid"); return FABM_ERR_CONFIG; }
+  if (!std::isfinite(p->alpha) || !(p->alpha > 0.0 && p->alpha <= 1.0)) {
+    set_status(status, FABM_ERR_CONFIG, "alpha must lie in (0, 1], got %.17g", p->alpha);
+    return FABM_ERR_CONFIG;
+  }
+  if (!system_dim_ok(p->system, p->dim)) {
+    set_status(status, FABM_ERR_CONFIG, "system %d does not support dim %d (device engine: dim <= %d)",
+               p->system, p->dim, FABM_MAX_DIM);
+    return FABM_ERR_CONFIG;
+  }
+  for (int i = 0; i < p->dim; ++i)
+    if (!std::isfinite(p->y0[i])) { set_status(status, FABM_ERR_CONFIG, "y0 must be finite"); return FABM_ERR_CONFIG; }
+  if (g->n_steps < 1) { set_status(status, FABM_ERR_CONFIG, "n_steps must be >= 1"); return FABM_ERR_CONFIG; }
+  if (!std::isfinite(g->h) || !(g->h > 0.0)) {
+    set_status(status, FABM_ERR_CONFIG, "step size must be finite and positive, got %.17g", g->h);
+    return FABM_ERR_CONFIG;
+  }
+  return FABM_OK;
+}
+
+// per-solve scalars, filled from libm when the caller left them zero
+void fill_scalars(const fabm_problem* p, fabm_grid* g) {
+  if (g->h_alpha == 0.0) g->h_alpha = std::pow(g->h, p->alpha);
+  if (g->gamma1 == 0.0) g->gamma1 = std::tgamma(p->alpha + 1.0);
+  if (g->gamma2 == 0.0) g->gamma2 = std::tgamma(p->alpha + 2.0);
+  if (g->inv_gamma2 == 0.0) g->inv_gamma2 = 1.0 / g->gamma2;
+}
+
+using EngineLaunch = cudaError_t (*)(const EngineParams&, int grid, cudaStream_t);
+
+template <int SYS, int D>
+cudaError_t launch_engine(const EngineParams& P, int grid, cudaStream_t stream) {
+  auto kern = abm_engine_kernel<SYS, D>;
+  const size_t smem = engine_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  EngineParams Pc = P;
+  void* args[] = {&Pc};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kThreads), args, smem, stream);
+}
+
+template <int SYS, int D>
+cudaError_t engine_occupancy(int* blocks_per_sm) {
+  auto kern = abm_engine_kernel<SYS, D>;
+  const size_t smem = engine_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, kThreads, smem);
+}
+
+EngineLaunch pick_engine(int sys, int dim) {
+  switch (sys) {
+    case FABM_SYS_CONSTANT:
+      switch (dim) {
+        case 1: return launch_engine<SYS_CONSTANT, 1>;
+        case 2: return launch_engine<SYS_CONSTANT, 2>;
+        case 3: return launch_engine<SYS_CONSTANT, 3>;
+        case 4: return launch_engine<SYS_CONSTANT, 4>;
+      }
+      break;
+    case FABM_SYS_LINEAR:
+      switch (dim) {
+        case 1: return launch_engine<SYS_LINEAR, 1>;
+        case 2: return launch_engine<SYS_LINEAR, 2>;
+        case 3: return launch_engine<SYS_LINEAR, 3>;
+        case 4: return launch_engine<SYS_LINEAR, 4>;
+      }
+      break;
+    case FABM_SYS_POWER_LAW: return launch_engine<SYS_POWER_LAW, 1>;
+    case FABM_SYS_HINDMARSH_ROSE: return launch_engine<SYS_HINDMARSH_ROSE, 3>;
+    case FABM_SYS_LORENZ: return launch_engine<SYS_LORENZ, 3>;
+    case FABM_SYS_CHEN: return launch_engine<SYS_CHEN, 3>;
+    case FABM_SYS_ROSSLER: return launch_engine<SYS_ROSSLER, 3>;
+    case FABM_SYS_FINANCIAL: return launch_engine<SYS_FINANCIAL, 3>;
+  }
+  return nullptr;
+}
+
+int stride_of(int dim) { return dim == 1 ? 1 : (dim == 2 ? 2 : 4); }
+
+}  // namespace
+
+struct fabm_plan {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  fabm_problem prob{};
+  fabm_grid grid{};
+  long long N = 0;
+  int nb = 0;
+  int ds = 1;
+  long long wlen = 0;
+  double* wb = nullptr;
+  double* wa = nullptr;
+  double* wc = nullptr;
+  double* y0 = nullptr;
+  double* Y = nullptr;
+  double* F = nullptr;
+  double* BK = nullptr;
+  int* ready = nullptr;
+  DevCtrl* ctrl = nullptr;
+  bool weights_ready = false;
+  int weights_mode = FABM_WEIGHTS_ACCURATE;
+  int bulk_ctas = 0;
+  EngineLaunch launch = nullptr;
+  fabm_stats stats{};
+};
+
+static void plan_free(fabm_plan* p) {
+  if (!p) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  for (void* ptr : {(void*)p->wb, (void*)p->wa, (void*)p->wc, (void*)p->y0, (void*)p->Y, (void*)p->F,
+                    (void*)p->BK, (void*)p->ready, (void*)p->ctrl})
+    if (ptr) cudaFree(ptr);
+  for (auto& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  cudaSetDevice(prev);
+  delete p;
+}
+
+extern "C" {
+
+const char* fabm_version(void) { return kVersion; }
+
+int fabm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid_in, int device, fabm_status* status) {
+  clear_status(status);
+  if (validate(problem, grid_in, status) != FABM_OK) return nullptr;
+  int ndev = fabm_device_count();
+  if (ndev <= 0 || device < 0 || device >= ndev) {
+    set_status(status, FABM_ERR_NODEVICE, "no CUDA device %d (found %d)", device, ndev);
+    return nullptr;
+  }
+  auto* p = new fabm_plan();
+  p->device = device;
+  p->prob = *problem;
+  p->grid = *grid_in;
+  fill_scalars(problem, &p->grid);
+  p->N = grid_in->n_steps;
+  p->nb = static_cast<int>((p->N + kB - 1) / kB);
+  p->ds = stride_of(problem->dim);
+  p->wlen = static_cast<long long>(p->nb) * kB + 2 * kB;
+  p->launch = pick_engine(problem->system, problem->dim);
+  auto fail = [&](const char* what, cudaError_t e) -> fabm_plan* {
+    set_status(status, FABM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    plan_free(p);
+    return nullptr;
+  };
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail("cudaSetDevice", e);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    set_status(status, FABM_ERR_NODEVICE, "device %d is sm_%d%d; libfabm is built for sm_100a", device, prop.major,
+               prop.minor);
+    plan_free(p);
+    return nullptr;
+  }
+  p->num_sms = prop.multiProcessorCount;
+  // bulk agents: 16 per CTA, one CTA per SM besides the stepper
+  const int n_targets = p->nb - kL;
+  if (n_targets > 0) {
+    int ctas = (n_targets + kWarps - 1) / kWarps;
+    ctas = std::min(ctas, p->num_sms - 1);
+    p->bulk_ctas = std::max(ctas, 1);
+    const int n_agents = p->bulk_ctas * kWarps;
+    if ((n_targets + n_agents - 1) / n_agents > kMaxOwn) {
+      set_status(status, FABM_ERR_CONFIG, "n_steps=%lld exceeds the engine capacity", p->N);
+      plan_free(p);
+      return nullptr;
+    }
+  }
+  if ((e = cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking)) != cudaSuccess) return fail("stream", e);
+  for (auto& ev : p->ev)
+    if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail("event", e);
+  const size_t wbytes = sizeof(double) * p->wlen;
+  const size_t fl = static_cast<size_t>(p->nb + 1) * kB * p->ds;
+  if ((e = cudaMalloc(&p->wb, wbytes)) != cudaSuccess) return fail("malloc b", e);
+  if ((e = cudaMalloc(&p->wa, wbytes)) != cudaSuccess) return fail("malloc a", e);
+  if ((e = cudaMalloc(&p->wc, wbytes)) != cudaSuccess) return fail("malloc c", e);
+  if ((e = cudaMalloc(&p->y0, sizeof(double) * FABM_MAX_DIM)) != cudaSuccess) return fail("malloc y0", e);
+  if ((e = cudaMalloc(&p->Y, sizeof(double) * (p->N + 1) * problem->dim)) != cudaSuccess) return fail("malloc Y", e);
+  if ((e = cudaMalloc(&p->F, sizeof(double) * fl)) != cudaSuccess) return fail("malloc F", e);
+  if ((e = cudaMalloc(&p->BK, sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds)) != cudaSuccess)
+    return fail("malloc BK", e);
+  if ((e = cudaMalloc(&p->ready, sizeof(int) * (p->nb + 1))) != cudaSuccess) return fail("malloc ready", e);
+  if ((e = cudaMalloc(&p->ctrl, sizeof(DevCtrl))) != cudaSuccess) return fail("malloc ctrl", e);
+  cudaMemsetAsync(p->F, 0, sizeof(double) * fl, p->stream);
+  cudaMemsetAsync(p->wb, 0, wbytes, p->stream);
+  cudaMemsetAsync(p->wa, 0, wbytes, p->stream);
+  cudaMemsetAsync(p->wc, 0, wbytes, p->stream);
+  cudaMemcpyAsync(p->y0, problem->y0, sizeof(double) * problem->dim, cudaMemcpyHostToDevice, p->stream);
+  if ((e = cudaStreamSynchronize(p->stream)) != cudaSuccess) return fail("init", e);
+  p->stats.block = kB;
+  p->stats.window_blocks = kL;
+  p->stats.bulk_ctas = p->bulk_ctas;
+  return p;
+}
+
+int fabm_plan_set_weights(fabm_plan* p, int mode, const double* b, const double* a, const double* c,
+                          fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  const long long n1 = p->N + 1;
+  if (mode == FABM_WEIGHTS_HOST) {
+    if (!b || !a || !c) { set_status(status, FABM_ERR_CONFIG, "host weights need b, a and c"); return FABM_ERR_CONFIG; }
+    // indices > N are never combined with a live history term; keep them 0
+    CUDA_TRY(cudaMemsetAsync(p->wb, 0, sizeof(double) * p->wlen, p->stream));
+    CUDA_TRY(cudaMemsetAsync(p->wa, 0, sizeof(double) * p->wlen, p->stream));
+    CUDA_TRY(cudaMemsetAsync(p->wc, 0, sizeof(double) * p->wlen, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(p->wb, b, sizeof(double) * n1, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(p->wa, a, sizeof(double) * n1, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(p->wc, c, sizeof(double) * n1, cudaMemcpyHostToDevice, p->stream));
+    p->stats.weights_ms = 0.0;
+  } else if (mode == FABM_WEIGHTS_ACCURATE || mode == FABM_WEIGHTS_FORMULA) {
+    CUDA_TRY(cudaEventRecord(p->ev[2], p->stream));
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<long long>((p->wlen + threads - 1) / threads, 148LL * 16));
+    weights_kernel<<<blocks, threads, 0, p->stream>>>(p->prob.alpha, p->grid.gamma1, p->grid.gamma2, p->wlen,
+                                                      mode == FABM_WEIGHTS_FORMULA ? 1 : 0, p->wb, p->wa, p->wc);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(p->ev[3], p->stream));
+    CUDA_TRY(cudaEventSynchronize(p->ev[3]));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p->ev[2], p->ev[3]);
+    p->stats.weights_ms = ms;
+  } else {
+    set_status(status, FABM_ERR_CONFIG, "unknown weight mode %d", mode);
+    return FABM_ERR_CONFIG;
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->weights_ready = true;
+  p->weights_mode = mode;
+  return FABM_OK;
+}
+
+int fabm_plan_set_y0(fabm_plan* p, const double* y0, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if (!y0) return FABM_OK;
+  for (int i = 0; i < p->prob.dim; ++i) {
+    if (!std::isfinite(y0[i])) { set_status(status, FABM_ERR_CONFIG, "y0 must be finite"); return FABM_ERR_CONFIG; }
+    p->prob.y0[i] = y0[i];
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaMemcpyAsync(p->y0, p->prob.y0, sizeof(double) * p->prob.dim, cudaMemcpyHostToDevice, p->stream));
+  return FABM_OK;
+}
+
+int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if (!p->launch) { set_status(status, FABM_ERR_CONFIG, "no engine for system/dim"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!p->weights_ready) {
+    int rc = fabm_plan_set_weights(p, FABM_WEIGHTS_ACCURATE, nullptr, nullptr, nullptr, status);
+    if (rc != FABM_OK) return rc;
+  }
+  CUDA_TRY(cudaMemsetAsync(p->ctrl, 0, sizeof(DevCtrl), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->ready, 0, sizeof(int) * (p->nb + 1), p->stream));
+  EngineParams P{};
+  P.N = p->N;
+  P.h = p->grid.h;
+  P.ha = p->grid.h_alpha;
+  P.ig = p->grid.inv_gamma2;
+  P.wb = p->wb;
+  P.wa = p->wa;
+  P.wc = p->wc;
+  P.y0 = p->y0;
+  P.Y = p->Y;
+  P.F = p->F;
+  P.BK = p->BK;
+  P.ready = p->ready;
+  P.ctrl = p->ctrl;
+  std::memcpy(P.params, p->prob.params, sizeof(P.params));
+  P.nb = p->nb;
+  P.n_agents = p->bulk_ctas * kWarps;
+  const double tmo = timeout_s > 0 ? timeout_s : 60.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  const int grid = 1 + p->bulk_ctas;
+  CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
+  CUDA_TRY(p->launch(P, grid, p->stream));
+  CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
+  CUDA_TRY(cudaEventSynchronize(p->ev[1]));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]);
+  DevCtrl h{};
+  CUDA_TRY(cudaMemcpy(&h, p->ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost));
+  p->stats.kernel_ms = ms;
+  p->stats.steps = p->N;
+  p->stats.history_fma = static_cast<int64_t>(p->prob.dim) * p->N * p->N;
+  p->stats.bulk_tiles = static_cast<int64_t>(h.bulk_tiles);
+  p->stats.leader_wait_ns = static_cast<int64_t>(h.leader_wait_ns);
+  if (h.err_code != ERR_OK) {
+    if (status) {
+      status->code = h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;
+      status->kind = h.err_kind;
+      status->step = h.err_step;
+      status->t = h.err_t;
+      if (h.err_code == ERR_TIMEOUT)
+        snprintf(status->message, sizeof(status->message), "device watchdog expired (no progress for %.1f s)", tmo);
+      else
+        snprintf(status->message, sizeof(status->message), "rhs returned a non-finite value");
+    }
+    return h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;
+  }
+  return FABM_OK;
+}
+
+int fabm_plan_download(fabm_plan* p, double* states, double* f_cache, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int d = p->prob.dim;
+  if (states)
+    CUDA_TRY(cudaMemcpyAsync(states, p->Y, sizeof(double) * (p->N + 1) * d, cudaMemcpyDeviceToHost, p->stream));
+  if (f_cache)
+    CUDA_TRY(cudaMemcpy2DAsync(f_cache, sizeof(double) * d, p->F, sizeof(double) * p->ds, sizeof(double) * d,
+                               p->N + 1, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return FABM_OK;
+}
+
+int fabm_plan_download_last(fabm_plan* p, double* y_last, fabm_status* status) {
+  clear_status(status);
+  if (!p || !y_last) { set_status(status, FABM_ERR_CONFIG, "null plan/output"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  const int d = p->prob.dim;
+  CUDA_TRY(cudaMemcpyAsync(y_last, p->Y + p->N * d, sizeof(double) * d, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return FABM_OK;
+}
+
+int fabm_plan_stats(const fabm_plan* p, fabm_stats* s) {
+  if (!p || !s) return FABM_ERR_CONFIG;
+  *s = p->stats;
+  return FABM_OK;
+}
+
+void fabm_plan_destroy(fabm_plan* p) { plan_free(p); }
+
+int fabm_solve(const fabm_problem* problem, const fabm_grid* grid, int weight_mode, const double* b,
+               const double* a, const double* c, double* states, double* f_cache, fabm_status* status) {
+  fabm_plan* p = fabm_plan_create(problem, grid, 0, status);
+  if (!p) return status ? status->code : FABM_ERR_CONFIG;
+  int rc = fabm_plan_set_weights(p, weight_mode, b, a, c, status);
+  if (rc == FABM_OK) rc = fabm_plan_run(p, 60.0, status);
+  if (rc == FABM_OK) rc = fabm_plan_download(p, states, f_cache, status);
+  plan_free(p);
+  return rc;
+}
+
+int fabm_weights(double alpha, int64_t n_steps, int mode, double gamma1, double gamma2, double* b, double* a,
+                 double* c, fabm_status* status) {
+  clear_status(status);
+  if (!std::isfinite(alpha) || !(alpha > 0.0 && alpha <= 1.0)) {
+    set_status(status, FABM_ERR_CONFIG, "alpha must lie in (0, 1], got %.17g", alpha);
+    return FABM_ERR_CONFIG;
+  }
+  if (n_steps < 1) { set_status(status, FABM_ERR_CONFIG, "n_steps must be >= 1"); return FABM_ERR_CONFIG; }
+  if (mode != FABM_WEIGHTS_ACCURATE && mode != FABM_WEIGHTS_FORMULA) {
+    set_status(status, FABM_ERR_CONFIG, "fabm_weights generates on device: mode must be ACCURATE or FORMULA");
+    return FABM_ERR_CONFIG;
+  }
+  if (fabm_device_count() <= 0) { set_status(status, FABM_ERR_NODEVICE, "no CUDA device"); return FABM_ERR_NODEVICE; }
+  if (gamma1 == 0.0) gamma1 = std::tgamma(alpha + 1.0);
+  if (gamma2 == 0.0) gamma2 = std::tgamma(alpha + 2.0);
+  const long long len = n_steps + 1;
+  double *db = nullptr, *da = nullptr, *dc = nullptr;
+  CUDA_TRY(cudaMalloc(&db, sizeof(double) * len));
+  CUDA_TRY(cudaMalloc(&da, sizeof(double) * len));
+  CUDA_TRY(cudaMalloc(&dc, sizeof(double) * len));
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<long long>((len + threads - 1) / threads, 148LL * 16));
+  weights_kernel<<<blocks, threads>>>(alpha, gamma1, gamma2, len, mode == FABM_WEIGHTS_FORMULA ? 1 : 0, db, da, dc);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(b, db, sizeof(double) * len, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(a, da, sizeof(double) * len, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(c, dc, sizeof(double) * len, cudaMemcpyDeviceToHost);
+  cudaFree(db);
+  cudaFree(da);
+  cudaFree(dc);
+  if (e != cudaSuccess) { set_status(status, FABM_ERR_CUDA, "weights: %s", cudaGetErrorString(e)); return FABM_ERR_CUDA; }
+  return FABM_OK;
+}
+
+int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64_t count, int device, double* states,
+                     double* f_cache, double* kernel_ms, fabm_status* status) {
+  (void)problems; (void)grids; (void)count; (void)device; (void)states; (void)f_cache; (void)kernel_ms;
+  clear_status(status);
+  set_status(status, FABM_ERR_CONFIG, "batch engine not built");
+  return FABM_ERR_CONFIG;
+}
+
+// ---------------------------------------------------------------- DFMA peak
+static __global__ void dfma_peak_kernel(double* out, int iters, double x) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = x + i * threadIdx.x;
+  const double m = 1.0 + 1e-12 * (threadIdx.x & 7);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fma(acc[i], m, 1e-9);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += acc[i];
+  if (s == 123.456) out[0] = s;
+}
+
+double fabm_measure_dfma_peak(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return 0.0;
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  double* out = nullptr;
+  cudaMalloc(&out, sizeof(double));
+  const int threads = 512, blocks = prop.multiProcessorCount * 4, iters = 20000;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_peak_kernel<<<blocks, threads>>>(out, 200, 1.0);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    dfma_peak_kernel<<<blocks, threads>>>(out, iters, 1.0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double fmas = static_cast<double>(blocks) * threads * iters * 8.0;
+  return fmas / (best * 1e-3);
+}
+
+}  // extern "C"

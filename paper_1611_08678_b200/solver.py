@@ -1,0 +1,242 @@
+"""GPU strategy: the drop-in replacement for ``fodeabm.serial.solve_serial``.
+
+``solve_gpu(problem, grid)`` keeps the reference call (serial.py:114-176):
+same arguments, same ``Trajectory`` result (fresh read-only host arrays),
+same errors — ``ValueError`` for configuration problems, ``SolverStepError``
+with the failing loop index and t=(n+1)h for non-finite rhs output,
+``StrategyTimeoutError`` when the device watchdog fires.  The whole O(N^2)
+loop runs in one cooperative kernel on the device (csrc/engine.cuh); the
+host only validates, launches and copies the trajectory back.
+
+Weights (the ``precompute_weights`` seam, serial.py:130):
+  * ``"accurate"`` (default) — generated on the device, cancellation-free;
+  * ``"formula"``  — generated on the device with the reference expression;
+  * ``"reference"`` — this package's ``precompute_weights`` (bitwise equal
+    to the reference table), uploaded; the 1e-12 parity mode;
+  * any object with ``.b .a .c`` arrays of length >= N+1 (a ``WeightTable``).
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native as nat
+from .core import GridSpec, SolverStepError, StrategyTimeoutError, Trajectory, precompute_weights
+from .systems import device_system_of
+
+__all__ = ["solve_gpu", "GpuPlan", "device_count", "measure_dfma_peak", "STRATEGY_NAME"]
+
+STRATEGY_NAME = "gpu"
+# the reference watchdog default (_shm.py:35); FABM_TIMEOUT_S overrides it
+DEFAULT_TIMEOUT_S = float(os.environ.get("FABM_TIMEOUT_S", "60"))
+
+
+def device_count() -> int:
+    return int(nat.load().fabm_device_count())
+
+
+def measure_dfma_peak(device: int = 0) -> float:
+    """Measured FP64 FMA/s of a DFMA-bound microbenchmark on ``device``."""
+    return float(nat.load().fabm_measure_dfma_peak(int(device)))
+
+
+def _raise_status(st: nat.Status, h: float | None = None):
+    msg = st.message.decode(errors="replace")
+    if st.code == nat.FABM_ERR_NONFINITE:
+        if st.kind == 1:
+            raise SolverStepError("rhs returned a non-finite value", step=0, t=0.0)
+        raise SolverStepError("rhs returned a non-finite value", step=int(st.step), t=float(st.t))
+    if st.code == nat.FABM_ERR_TIMEOUT:
+        raise StrategyTimeoutError(msg or "device watchdog expired")
+    if st.code == nat.FABM_ERR_CONFIG:
+        raise ValueError(msg)
+    raise RuntimeError(f"libfabm error {st.code}: {msg}")
+
+
+def _structs(problem, grid):
+    tag = device_system_of(problem.rhs)
+    dim = int(problem.dim)
+    if tag.dim is not None and tag.dim != dim:
+        raise ValueError(f"rhs {tag.name!r} has dimension {tag.dim}, problem has dim {dim}")
+    if dim > nat.MAX_DIM:
+        raise ValueError(f"the device engine supports dim <= {nat.MAX_DIM}, got {dim}")
+    alpha = float(problem.alpha)
+    pr = nat.Problem()
+    pr.alpha = alpha
+    pr.dim = dim
+    pr.system = tag.system_id
+    for i, v in enumerate(tag.params[: nat.MAX_PARAMS]):
+        pr.params[i] = v
+    y0 = np.asarray(problem.y0, dtype=np.float64).reshape(-1)
+    for i in range(dim):
+        pr.y0[i] = float(y0[i])
+    gr = nat.Grid()
+    gr.n_steps = int(grid.n_steps)
+    gr.h = float(grid.h)
+    # the scalars of serial.py:135-136 / core.py:146-147, computed by CPython
+    gr.h_alpha = float(grid.h) ** alpha
+    gr.gamma1 = math.gamma(alpha + 1.0)
+    gr.gamma2 = math.gamma(alpha + 2.0)
+    gr.inv_gamma2 = 1.0 / math.gamma(alpha + 2.0)
+    return pr, gr, tag
+
+
+def _weight_arrays(weights, alpha: float, n_steps: int):
+    if isinstance(weights, str):
+        if weights == "accurate":
+            return nat.WEIGHTS_ACCURATE, None
+        if weights == "formula":
+            return nat.WEIGHTS_FORMULA, None
+        if weights == "reference":
+            table = precompute_weights(alpha, n_steps)
+        else:
+            raise ValueError(f"unknown weights mode {weights!r}")
+    else:
+        table = weights
+    arrs = []
+    for name in ("b", "a", "c"):
+        arr = np.ascontiguousarray(np.asarray(getattr(table, name), dtype=np.float64))
+        if arr.ndim != 1 or arr.shape[0] < n_steps + 1:
+            raise ValueError(f"weight table {name!r} needs at least {n_steps + 1} entries")
+        arrs.append(arr[: n_steps + 1].copy())
+    return nat.WEIGHTS_HOST, arrs
+
+
+class GpuPlan:
+    """Device-resident buffers for one (problem, grid) on one GPU.
+
+    Re-running a plan reuses the allocation and the device weight table;
+    ``run()`` times the engine kernel with CUDA events on the plan stream.
+    """
+
+    def __init__(self, problem, grid, *, weights="accurate", device: int = 0):
+        lib = nat.load()
+        self.problem = problem
+        self.grid = grid
+        self.device = int(device)
+        self._pr, self._gr, self.tag = _structs(problem, grid)
+        st = nat.Status()
+        handle = lib.fabm_plan_create(ctypes_ref(self._pr), ctypes_ref(self._gr), self.device, ctypes_ref(st))
+        if not handle:
+            _raise_status(st)
+        self._h = handle
+        self._lib = lib
+        self.weights_mode = None
+        self.set_weights(weights)
+
+    # -- configuration -------------------------------------------------
+    def set_weights(self, weights):
+        mode, arrs = _weight_arrays(weights, float(self.problem.alpha), int(self.grid.n_steps))
+        st = nat.Status()
+        ptrs = [nat.dptr(a) for a in arrs] if arrs else [None, None, None]
+        rc = self._lib.fabm_plan_set_weights(self._h, mode, *ptrs, ctypes_ref(st))
+        if rc != nat.FABM_OK:
+            _raise_status(st)
+        self.weights_mode = weights if isinstance(weights, str) else "table"
+
+    def set_y0(self, y0):
+        y0 = np.ascontiguousarray(np.asarray(y0, dtype=np.float64).reshape(-1))
+        st = nat.Status()
+        if self._lib.fabm_plan_set_y0(self._h, nat.dptr(y0), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    # -- execution -----------------------------------------------------
+    def run(self, timeout_s: float = DEFAULT_TIMEOUT_S) -> float:
+        """Run the engine; returns the kernel time in ms (CUDA events)."""
+        st = nat.Status()
+        if self._lib.fabm_plan_run(self._h, float(timeout_s), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st, self.grid.h)
+        return self.stats()["kernel_ms"]
+
+    def download(self) -> Trajectory:
+        N, d = int(self.grid.n_steps), int(self.problem.dim)
+        states = np.empty((N + 1, d))
+        f_cache = np.empty((N + 1, d))
+        st = nat.Status()
+        if self._lib.fabm_plan_download(self._h, nat.dptr(states), nat.dptr(f_cache), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+        grid = self.grid if isinstance(self.grid, GridSpec) else GridSpec(self.grid.n_steps, self.grid.h)
+        return Trajectory(grid=grid, states=states, f_cache=f_cache)
+
+    def last_state(self) -> np.ndarray:
+        out = np.empty(int(self.problem.dim))
+        st = nat.Status()
+        if self._lib.fabm_plan_download_last(self._h, nat.dptr(out), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+        return out
+
+    def stats(self) -> dict:
+        s = nat.Stats()
+        self._lib.fabm_plan_stats(self._h, ctypes_ref(s))
+        return s.as_dict()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.fabm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ctypes_ref(obj):
+    import ctypes
+
+    return ctypes.byref(obj)
+
+
+_PLAN_CACHE: "OrderedDict[tuple, GpuPlan]" = OrderedDict()
+_PLAN_CACHE_SIZE = 2
+
+
+def _cached_plan(problem, grid, weights, device) -> GpuPlan:
+    tag = device_system_of(problem.rhs)
+    wkey = weights if isinstance(weights, str) else id(weights)
+    key = (device, tag, int(problem.dim), float(problem.alpha), int(grid.n_steps), float(grid.h), wkey)
+    plan = _PLAN_CACHE.get(key)
+    if plan is not None and isinstance(weights, str):
+        _PLAN_CACHE.move_to_end(key)
+        plan.problem = problem
+        return plan
+    plan = GpuPlan(problem, grid, weights=weights, device=device)
+    if isinstance(weights, str):
+        _PLAN_CACHE[key] = plan
+        while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+            _PLAN_CACHE.popitem(last=False)[1].close()
+    return plan
+
+
+def solve_gpu(
+    problem,
+    grid,
+    *,
+    weights="accurate",
+    device: int = 0,
+    timeout_s: float = DEFAULT_TIMEOUT_S,
+    stats: dict | None = None,
+) -> Trajectory:
+    """Integrate ``problem`` over ``grid`` on the GPU (drop-in for solve_serial).
+
+    Deterministic: identical inputs give bitwise-identical trajectories.
+    """
+    N = int(grid.n_steps)
+    if not grid.spans(problem.t_end):
+        raise ValueError(f"grid (h={grid.h!r}, N={N}) does not span t_end={problem.t_end!r}")
+    device_system_of(problem.rhs)
+    # shape and finiteness of f(0, y0), exactly as the reference validates it
+    problem.eval_rhs0()
+    plan = _cached_plan(problem, grid, weights, device)
+    plan.set_y0(problem.y0)
+    plan.run(timeout_s)
+    traj = plan.download()
+    if stats is not None:
+        stats.update(plan.stats())
+        stats["strategy"] = STRATEGY_NAME
+    return traj

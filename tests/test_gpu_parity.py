@@ -1,0 +1,189 @@
+"""GPU parity: the device engine (via the C ABI, libfabm.so) against the
+reference's own trajectories (tests/golden/) and the CPU oracle.
+
+Tolerance contract (BASELINE.json north_star):
+  * reference weight table injected  -> <= 1e-12 normwise relative
+  * device ACCURATE weights           -> <= 1e-12 vs the oracle run with the
+                                         same accurate table injected
+  * closed form (C1 Mittag-Leffler)  -> discretisation error bounds
+Bitwise: repeat solves, and the prefix of a long run vs the short run.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import TRAJ_FIXTURES, golden, golden_errors, normwise_dev, problem_from_golden, sup_rel_dev
+from oracle import abm_oracle, c_oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.mark.parametrize("name", TRAJ_FIXTURES)
+def test_reference_table_parity(fabm, name):
+    g = golden(name)
+    problem, grid = problem_from_golden(g)
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    rows = g["rows"]
+    assert normwise_dev(traj.states[rows], g["states"]) <= TOL
+    assert normwise_dev(traj.f_cache[rows], g["f_cache"]) <= TOL
+    assert traj.states.shape == (grid.n_steps + 1, problem.dim)
+    assert not traj.states.flags.writeable
+
+
+def test_c2_lorenz_full_parity(fabm):
+    """BASELINE config 2 (Lorenz a=0.99, T=100, N=1e5), non-chaotic: full horizon."""
+    g = golden("c2_lorenz_full")
+    problem, grid = problem_from_golden(g)
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    rows = g["rows"]
+    assert normwise_dev(traj.states[rows], g["states"]) <= TOL
+    np.testing.assert_allclose(traj.states[-1], [-8.4841261, -8.48133593, 27.00215473], rtol=1e-7)
+
+
+def test_c1_mittag_leffler(fabm):
+    g = golden("c1_linear")
+    problem, grid = problem_from_golden(g)
+    traj = fabm.solve_gpu(problem, grid)  # device ACCURATE weights
+    t = grid.times()[::50]
+    exact = np.array([abm_oracle.mittag_leffler(0.8, -(ti ** 0.8)) for ti in t])
+    err = np.abs(traj.states[::50, 0] - exact)
+    assert err.max() <= 4e-5
+    assert abs(traj.states[-1, 0] - 0.042979301317701527263) <= 1e-6
+
+
+@pytest.mark.parametrize("alpha", [0.3, 0.5, 0.9, 0.99, 1.0])
+def test_device_weights_vs_mpmath(fabm, alpha):
+    import ctypes
+
+    from paper_1611_08678_b200 import _native as nat
+
+    lib = nat.load()
+    N = 10**6
+    b = np.empty(N + 1)
+    a = np.empty(N + 1)
+    c = np.empty(N + 1)
+    st = nat.Status()
+    rc = lib.fabm_weights(alpha, N, nat.WEIGHTS_ACCURATE, math.gamma(alpha + 1.0), math.gamma(alpha + 2.0),
+                          nat.dptr(b), nat.dptr(a), nat.dptr(c), ctypes.byref(st))
+    assert rc == 0, st.message
+    idx = np.array([0, 1, 2, 3, 4, 7, 8, 15, 16, 100, 1234, 10**4, 10**5, 10**6])
+    exact = abm_oracle.exact_weights(alpha, idx)
+    got = np.stack([b[idx], a[idx], c[idx]], axis=1)
+    assert (np.abs(got - exact) / np.abs(exact)).max() <= 8e-15
+    # the formula mode reproduces the reference expression to pow rounding
+    rc = lib.fabm_weights(alpha, 2000, nat.WEIGHTS_FORMULA, math.gamma(alpha + 1.0), math.gamma(alpha + 2.0),
+                          nat.dptr(b), nat.dptr(a), nat.dptr(c), ctypes.byref(st))
+    assert rc == 0
+    rb, ra, rc_ = abm_oracle.reference_weights(alpha, 2000)
+    np.testing.assert_allclose(b[:2001], rb, rtol=1e-11)
+    np.testing.assert_allclose(c[:2001], rc_, rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["lorenz_prefix", "hindmarsh_rose", "financial_4095"])
+def test_accurate_weights_vs_oracle(fabm, name):
+    g = golden(name)
+    problem, grid = problem_from_golden(g)
+    traj = fabm.solve_gpu(problem, grid, weights="accurate")
+    w = abm_oracle.accurate_weights(problem.alpha, grid.n_steps)
+    ref, _ = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, grid.n_steps, weights=w)
+    assert normwise_dev(traj.states, ref) <= TOL
+
+
+def test_determinism_bitwise(fabm):
+    problem = fabm.FractionalProblem(alpha=0.99, dim=3, rhs=fabm.rhs_lorenz(), y0=(1.0, 1.0, 1.0), t_end=20.0)
+    grid = problem.grid(20000)
+    a = fabm.solve_gpu(problem, grid)
+    b = fabm.solve_gpu(problem, grid)
+    assert np.array_equal(a.states, b.states)
+    assert np.array_equal(a.f_cache, b.f_cache)
+
+
+def test_prefix_of_long_run_is_bitwise(fabm):
+    """The first M steps of an N-step run equal the M-step run."""
+    lor = fabm.rhs_lorenz()
+    long = fabm.FractionalProblem(alpha=0.99, dim=3, rhs=lor, y0=(1.0, 1.0, 1.0), t_end=10.0)
+    grid = fabm.GridSpec(n_steps=100000, h=1e-4)
+    full = fabm.solve_gpu(long, grid)
+    M = 7777
+    short = fabm.FractionalProblem(alpha=0.99, dim=3, rhs=lor, y0=(1.0, 1.0, 1.0), t_end=M * 1e-4)
+    pre = fabm.solve_gpu(short, fabm.GridSpec(n_steps=M, h=1e-4))
+    assert np.array_equal(full.states[: M + 1], pre.states)
+
+
+def test_large_n_vs_c_oracle(fabm):
+    """N = 3e4 Lorenz on the C1e-4 grid: engine vs the C oracle (same accurate table)."""
+    lor = fabm.rhs_lorenz()
+    N = 30000
+    problem = fabm.FractionalProblem(alpha=0.99, dim=3, rhs=lor, y0=(1.0, 1.0, 1.0), t_end=N * 1e-4)
+    grid = fabm.GridSpec(n_steps=N, h=1e-4)
+    traj = fabm.solve_gpu(problem, grid)
+    w = abm_oracle.accurate_weights(problem.alpha, N)
+    ref, fref = c_oracle.solve("lorenz", lor.device_system.params, problem.alpha, problem.y0, grid.h, N, w,
+                               threads=c_oracle.max_threads())
+    assert normwise_dev(traj.states, ref) <= TOL
+    assert normwise_dev(traj.f_cache, fref) <= TOL
+
+
+@pytest.mark.parametrize("name", ["overflow", "initial"])
+def test_error_step_matches_reference(fabm, name):
+    errs = golden_errors()
+    lam, y0, N = errs[name + "_config"]
+    step, t = errs[name]
+    problem = fabm.FractionalProblem(alpha=0.8, dim=1, rhs=fabm.rhs_linear(lam), y0=[y0], t_end=1.0)
+    with np.errstate(over="ignore", invalid="ignore"):
+        with pytest.raises(fabm.SolverStepError) as info:
+            fabm.solve_gpu(problem, problem.grid(N), weights="reference")
+    assert info.value.step == step
+    assert info.value.t == pytest.approx(t, rel=1e-15)
+
+
+def test_constant_preservation_bitwise(fabm):
+    # pkg/tests/test_serial.py:112-116
+    problem = fabm.FractionalProblem(alpha=0.5, dim=2, rhs=fabm.rhs_constant([0.0, 0.0]), y0=(3.0, -1.5), t_end=1.0)
+    traj = fabm.solve_gpu(problem, problem.grid(2000))
+    assert (traj.states == np.array([3.0, -1.5])).all()
+    assert (traj.f_cache == 0.0).all()
+
+
+def test_alpha_one_exact(fabm):
+    # pkg/tests/test_serial.py:118-123 — alpha = 1, constant rhs: y = 1 + 2.5 t
+    problem = fabm.FractionalProblem(alpha=1.0, dim=1, rhs=fabm.rhs_constant([2.5]), y0=(1.0,), t_end=2.0)
+    grid = problem.grid(1000)
+    traj = fabm.solve_gpu(problem, grid)
+    np.testing.assert_allclose(traj.states[:, 0], 1.0 + 2.5 * grid.times(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 127, 128, 129, 383, 384, 385, 512, 641])
+def test_edge_sizes(fabm, N):
+    """Step counts around the block (128) and window (3 blocks) boundaries."""
+    problem = fabm.FractionalProblem(alpha=0.7, dim=1, rhs=fabm.rhs_linear(-0.5), y0=[1.0], t_end=1.0)
+    grid = problem.grid(N)
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    ref, fref = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, N)
+    assert sup_rel_dev(traj.states, ref) <= 1e-12
+    assert sup_rel_dev(traj.f_cache, fref) <= 1e-12
+
+
+def test_plain_callable_rejected(fabm):
+    problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=lambda t, y: (0.0,), y0=[0.0], t_end=1.0)
+    with pytest.raises(ValueError):
+        fabm.solve_gpu(problem, problem.grid(10))
+
+
+def test_accepts_reference_style_objects(fabm):
+    """Duck-typed problem/grid objects (e.g. fodeabm's own) are accepted."""
+    from types import SimpleNamespace
+
+    rhs = fabm.rhs_linear(-1.0)
+    p = SimpleNamespace(alpha=0.8, dim=1, rhs=rhs, y0=np.array([1.0]), t_end=10.0,
+                        eval_rhs0=lambda: np.array([-1.0]))
+    grid = fabm.GridSpec(n_steps=1000, h=0.01)
+    traj = fabm.solve_gpu(p, grid, weights="reference")
+    g = golden("c1_linear")
+    assert normwise_dev(traj.states, g["states"]) <= TOL

@@ -1,0 +1,152 @@
+"""Host-side API mirror of fodeabm (no GPU needed): types, validation,
+weights seam, rhs expressions and device tags."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+import paper_1611_08678_b200 as fabm
+from paper_1611_08678_b200.systems import SYSTEM_IDS, device_system_of
+
+
+class TestProblemValidation:
+    # mirrors pkg/tests/test_serial.py:202-225
+    def test_alpha_range(self):
+        for alpha in (0.0, -0.2, 1.0001, float("nan")):
+            with pytest.raises(ValueError):
+                fabm.FractionalProblem(alpha=alpha, dim=1, rhs=fabm.rhs_constant([0.0]), y0=[0.0], t_end=1.0)
+
+    def test_dimension_mismatch(self):
+        with pytest.raises(ValueError):
+            fabm.FractionalProblem(alpha=0.5, dim=2, rhs=fabm.rhs_constant([0.0, 0.0]), y0=[0.0], t_end=1.0)
+
+    def test_rhs_output_shape_checked(self):
+        problem = fabm.FractionalProblem(alpha=0.5, dim=2, rhs=fabm.rhs_constant([0.0]), y0=[0.0, 0.0], t_end=1.0)
+        with pytest.raises(ValueError):
+            problem.eval_rhs0()
+
+    def test_horizon_positive(self):
+        with pytest.raises(ValueError):
+            fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_constant([0.0]), y0=[0.0], t_end=0.0)
+
+    def test_y0_finite_and_read_only(self):
+        with pytest.raises(ValueError):
+            fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_constant([0.0]), y0=[np.inf], t_end=1.0)
+        p = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_constant([0.0]), y0=[1.0], t_end=1.0)
+        with pytest.raises(ValueError):
+            p.y0[0] = 2.0
+
+    def test_grid(self):
+        g = fabm.GridSpec.from_horizon(2.0, 4)
+        np.testing.assert_allclose(g.times(), [0.0, 0.5, 1.0, 1.5, 2.0])
+        assert g.spans(2.0)
+        assert not fabm.GridSpec(n_steps=10, h=0.5).spans(1.0)
+        with pytest.raises(ValueError):
+            fabm.GridSpec(n_steps=0, h=0.1)
+        with pytest.raises(ValueError):
+            fabm.GridSpec(n_steps=3, h=-0.1)
+
+    def test_nonfinite_initial_rhs_is_step_error(self):
+        p = fabm.FractionalProblem(alpha=0.8, dim=1, rhs=fabm.rhs_linear(1e300), y0=[1e300], t_end=1.0)
+        with np.errstate(over="ignore"):
+            with pytest.raises(fabm.SolverStepError) as info:
+                p.eval_rhs0()
+        assert info.value.step == 0 and info.value.t == 0.0
+
+
+class TestWeights:
+    @pytest.mark.parametrize("alpha", [0.3, 0.5, 0.77, 0.8, 0.9, 0.99, 1.0])
+    def test_table_bitwise_equals_reference(self, alpha):
+        g = golden("weights_ref")
+        t = fabm.precompute_weights(alpha, 500)
+        assert np.array_equal(t.b, g[f"b_{alpha}"])
+        assert np.array_equal(t.a, g[f"a_{alpha}"])
+        assert np.array_equal(t.c, g[f"c_{alpha}"])
+        assert not t.b.flags.writeable
+
+    def test_single_weight_functions_bitwise(self):
+        g = golden("weights_ref")
+        for al in (0.5, 0.99):
+            for i, n in enumerate(g["sample_index"]):
+                assert fabm.predictor_weight(al, int(n)) == g[f"sample_b_{al}"][i]
+                assert fabm.corrector_weight_a(al, int(n)) == g[f"sample_a_{al}"][i]
+                assert fabm.corrector_weight_c(al, int(n)) == g[f"sample_c_{al}"][i]
+
+    def test_validation(self):
+        with pytest.raises(ValueError):
+            fabm.precompute_weights(0.5, 0)
+        with pytest.raises(ValueError):
+            fabm.predictor_weight(1.5, 3)
+        with pytest.raises(ValueError):
+            fabm.corrector_weight_a(0.5, -1)
+        assert fabm.gamma(0.5) == pytest.approx(1.7724538509055160273, rel=1e-13)
+        with pytest.raises(ValueError):
+            fabm.gamma(0.0)
+
+
+class TestSystems:
+    def test_known_values(self):
+        # pkg/tests/test_systems.py:8,26-31,64-67
+        assert fabm.rhs_power_law(0.5, 2.0)(1.0, None)[0] == pytest.approx(1.5045055561273500985, rel=1e-14)
+        assert fabm.rhs_power_law(0.5, 2.0)(0.0, None)[0] == 0.0
+        np.testing.assert_allclose(fabm.rhs_hindmarsh_rose()(0.0, (0.0, 0.0, 0.0)), (3.25, 1.0, 0.0384), rtol=1e-14)
+        np.testing.assert_allclose(fabm.rhs_lorenz()(0.0, (1.0, 1.0, 1.0)), (0.0, 26.0, 1.0 - 8.0 / 3.0))
+        assert fabm.rhs_rossler()(0.0, (0.0, 0.0, 0.0)) == (0.0, 0.0, 0.2)
+        assert fabm.rhs_financial()(0.0, (0.0, 0.0, 0.0)) == (0.0, 1.0, 0.0)
+        assert fabm.rhs_chen()(0.0, (1.0, 1.0, 1.0)) == (0.0, -7.0 - 1.0 + 28.0, 1.0 - 3.0)
+
+    def test_power_law_with_beta_equal_alpha_is_constant(self):
+        f = fabm.rhs_power_law(0.5, 0.5)
+        assert device_system_of(f).name == "constant"
+        assert f(2.0, None)[0] == pytest.approx(math.gamma(1.5), rel=1e-15)
+
+    def test_device_tags(self):
+        for fn, name in ((fabm.rhs_lorenz(), "lorenz"), (fabm.rhs_chen(), "chen"), (fabm.rhs_rossler(), "rossler"),
+                         (fabm.rhs_financial(), "financial"), (fabm.rhs_hindmarsh_rose(), "hindmarsh-rose"),
+                         (fabm.rhs_linear(-1.0), "linear"), (fabm.rhs_constant([1.0, 2.0]), "constant")):
+            tag = device_system_of(fn)
+            assert tag.name == name
+            assert tag.system_id == SYSTEM_IDS[name]
+
+    def test_plain_callable_has_no_device_tag(self):
+        with pytest.raises(ValueError):
+            device_system_of(lambda t, y: y)
+
+    def test_rejects_bad_parameters(self):
+        with pytest.raises(ValueError):
+            fabm.rhs_linear(float("nan"))
+        with pytest.raises(ValueError):
+            fabm.rhs_constant([float("inf")])
+        with pytest.raises(ValueError):
+            fabm.rhs_power_law(0.8, 0.3)
+        with pytest.raises(ValueError):
+            fabm.HindmarshRoseParams(r=0.0)
+        with pytest.raises(ValueError):
+            fabm.rhs_lorenz(sigma=float("nan"))
+
+
+class TestSolverFrontEnd:
+    """Checks solve_gpu performs before touching the device."""
+
+    def test_grid_must_span_horizon(self):
+        problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_constant([0.0]), y0=[0.0], t_end=1.0)
+        with pytest.raises(ValueError):
+            fabm.solve_gpu(problem, fabm.GridSpec(n_steps=10, h=0.5))
+
+    def test_plain_callable_rejected(self):
+        problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=lambda t, y: (0.0,), y0=[0.0], t_end=1.0)
+        with pytest.raises(ValueError):
+            fabm.solve_gpu(problem, problem.grid(10))
+
+    def test_product_never_imports_oracle(self):
+        import pathlib
+
+        pkg = pathlib.Path(fabm.__file__).parent
+        for path in pkg.rglob("*.py"):
+            text = path.read_text()
+            assert "import oracle" not in text and "from oracle" not in text, path
