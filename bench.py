@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the ABM history engine on the BASELINE.json headline metric.
+
+Workload (BASELINE.json metric "Lorenz N=1e6"; SURVEY.md §8d "Headline"):
+fractional Lorenz (sigma, rho, beta) = (10, 28, 8/3), alpha = 0.99,
+y0 = (1, 1, 1), T = 100, N = 1e6 steps (h = 1e-4), FP64 throughout.
+A bench "step" is one full solve of that trajectory (all N ODE steps).
+
+  value      whole-job ODE steps/s = ranks * N / device time per solve
+             (engine kernel, CUDA events on the engine stream, inputs and
+             weights resident; L2 flushed between solves)
+  e2e        the same metric through the public call solve_gpu() with host
+             buffers: y0 H2D, device weight generation, engine, and the D2H
+             of the whole trajectory (states + f_cache) every step
+  roofline   history FP64 FMAs (d*N^2 per trajectory, 2 flop each) over the
+             engine time vs the DFMA peak measured live by a microbenchmark
+  cpu_baseline  the CPU port of the reference solver (oracle/abm_oracle.c,
+             OpenMP, all host threads) on a bounded prefix of the same run,
+             projected to N with the fitted cost model t = a*M + c*M^2
+
+Multi-GPU (torchrun): every rank integrates its own trajectory (weak
+scaling, "replicas" of the single-trajectory engine; y0 perturbed per rank);
+NCCL is used for the barrier, the max-over-ranks time and the final gather.
+
+--impl reference runs the CPU port alone (rank 0), as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_STEPS = 1_000_000
+T_END = 100.0
+ALPHA = 0.99
+Y0 = (1.0, 1.0, 1.0)
+METRIC = "ABM steps/sec, fractional Lorenz N=1e6 (alpha 0.99, T=100, d=3, FP64)"
+UNIT = "steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fabm", choices=["fabm", "reference"])
+    ap.add_argument("--n", type=int, default=N_STEPS, help="ODE steps per trajectory")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU sample budget")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def lorenz_problem(fabm, rank: int, n_steps: int):
+    y0 = (Y0[0] + 1e-3 * rank, Y0[1], Y0[2])
+    problem = fabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=fabm.rhs_lorenz(), y0=y0, t_end=T_END)
+    return problem, problem.grid(n_steps)
+
+
+def cpu_port_time(n_prefix: int, threads: int) -> float:
+    """Seconds for the CPU port (oracle/abm_oracle.c) on the first n_prefix steps."""
+    from oracle import abm_oracle, c_oracle
+
+    h = T_END / N_STEPS
+    w = abm_oracle.reference_weights(ALPHA, n_prefix)
+    t0 = time.perf_counter()
+    c_oracle.solve("lorenz", (10.0, 28.0, 8.0 / 3.0), ALPHA, Y0, h, n_prefix, w, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(n_target: int, budget_s: float) -> dict:
+    """Bounded CPU sample + two-point cost-model projection to n_target."""
+    from oracle import c_oracle
+
+    c_oracle.build()
+    threads = c_oracle.max_threads()
+    m1 = 4000
+    t1 = cpu_port_time(m1, threads)
+    # grow the prefix until one sample is ~budget/4, then a 2x prefix
+    while t1 < budget_s / 16 and m1 < n_target // 4:
+        m1 *= 2
+        t1 = cpu_port_time(m1, threads)
+    m2 = min(2 * m1, n_target)
+    t2 = cpu_port_time(m2, threads)
+    # t = a*M + c*M^2 through both samples
+    c = (t2 / m2 - t1 / m1) / (m2 - m1)
+    a = t1 / m1 - c * m1
+    if c <= 0:
+        c, a = t2 / (m2 * m2), 0.0
+    a = max(a, 0.0)
+    t_full = a * n_target + c * n_target * n_target
+    return {
+        "value": n_target / t_full,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"oracle/abm_oracle.c (C port of serial.py:150-170 with reduction.py-style per-thread spans), "
+                   f"{threads} OpenMP threads, Lorenz prefixes M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s) of the "
+                   f"N={n_target} run; projected t(N)=a*N+c*N^2 = {t_full:.1f}s"),
+        "projected_seconds": t_full,
+        "cpu_model": _cpu_model(),
+    }
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, value: float) -> float:
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    n = args.n
+    budget = args.cpu_seconds
+    times = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        info = cpu_baseline(n, budget / 2)
+        if i >= args.warmup:
+            times.append(info["projected_seconds"])
+    t_full = statistics.median(times)
+    value = n / t_full
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_full * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (deterministic Lorenz IVP)",
+        "config": {"workload": "fractional Lorenz alpha=0.99 T=100 N=1e6 single trajectory", "n_steps": n,
+                   "system": "lorenz", "alpha": ALPHA, "t_end": T_END},
+        "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def run_fabm(args, world, rank, local):
+    import torch
+
+    import paper_1611_08678_b200 as fabm
+
+    torch.cuda.set_device(local)
+    n = args.n
+    problem, grid = lorenz_problem(fabm, rank, n)
+    plan = fabm.GpuPlan(problem, grid, weights="accurate", device=local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        torch.cuda.synchronize()
+        plan.run()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    kernel_ms = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        kernel_ms.append(plan.run())
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t0
+    clocks = sampler.stop()
+    stats = plan.stats()
+    y_last = plan.last_state()
+    mean_ms = float(np.mean(kernel_ms))
+    step_ms = max_over_ranks(world, mean_ms)
+    value = world * n / (step_ms * 1e-3)
+
+    # ---- e2e: the public call with host buffers, every step
+    times = []
+    h2d = 8 * 3 + 8 * 16  # y0 + rhs params
+    d2h = 2 * (n + 1) * 3 * 8  # states + f_cache
+    fabm.solve_gpu(problem, grid)  # warm plan cache
+    barrier(world)
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        traj = fabm.solve_gpu(problem, grid)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t1)
+    e2e_s = max_over_ranks(world, float(np.mean(times)))
+    e2e_value = world * n / e2e_s
+    assert np.array_equal(traj.states[-1], y_last), "e2e and device-resident runs differ"
+
+    # ---- roofline: FP64 FMA pipe (measured DFMA peak on this GPU, live)
+    peak_fma = fabm.measure_dfma_peak(local)
+    hist_fma = 3.0 * n * n
+    achieved_tflops = 2.0 * hist_fma / (mean_ms * 1e-3) / 1e12
+    peak_tflops = 2.0 * peak_fma / 1e12
+    traffic = None
+    prof = ROOT / "profiles" / "engine_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    gathered = None
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor(y_last, dtype=torch.float64, device="cuda")
+        buf = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(buf, t)
+        gathered = [b.cpu().tolist() for b in buf]
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        info = cpu_baseline(n, args.cpu_seconds)
+        cpu = {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (deterministic Lorenz IVP; y0 perturbed 1e-3*rank per rank)",
+        "config": {
+            "workload": "fractional Lorenz alpha=0.99 T=100 N=1e6 single trajectory per GPU",
+            "n_steps": n, "system": "lorenz", "alpha": ALPHA, "t_end": T_END,
+            "weights": "device accurate (resident)", "l2": "flushed (256 MB write) before every timed solve",
+            "parallelism": f"replicas x{world}",
+        },
+        "history_fma_per_s": hist_fma / (mean_ms * 1e-3) * world,
+        "roofline": {
+            "bound": "fp64",
+            "achieved": achieved_tflops,
+            "peak": peak_tflops,
+            "unit": "TFLOP/s",
+            "frac": achieved_tflops / peak_tflops,
+            "traffic": traffic,
+            "note": ("history FP64 FMA pipe: 2*d*N^2 algorithmic flop per solve over the engine kernel time; "
+                     "peak = DFMA microbenchmark measured live (MEASURED_PEAKS.json has no FP64 entry)"),
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": len(kernel_ms),
+        "clocks": clocks,
+        "engine": {"kernel_ms": kernel_ms, "wall_s": wall, "bulk_ctas": stats["bulk_ctas"],
+                   "bulk_tiles": stats["bulk_tiles"], "leader_wait_ms": stats["leader_wait_ns"] / 1e6,
+                   "block": stats["block"], "window_blocks": stats["window_blocks"],
+                   "y_N": y_last.tolist(), "gathered_y_N": gathered},
+    }
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_fabm(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,6 +113,7 @@ typedef struct fabm_stats {
   int64_t history_fma;     /* algorithmic history FMAs per trajectory = d*N^2   */
   int64_t bulk_tiles;      /* Toeplitz tiles processed by the bulk agents       */
   int64_t leader_wait_ns;  /* time the stepper spent waiting on handoffs        */
+  int64_t leader_throttle_ns; /* time the stepper waited for ring consumers     */
   int32_t bulk_ctas;       /* CTAs running bulk agents                          */
   int32_t block;           /* history block B                                   */
   int32_t window_blocks;   /* stepper window L (blocks)                         */

@@ -90,6 +90,7 @@ class Stats(ctypes.Structure):
         ("history_fma", ctypes.c_int64),
         ("bulk_tiles", ctypes.c_int64),
         ("leader_wait_ns", ctypes.c_int64),
+        ("leader_throttle_ns", ctypes.c_int64),
         ("bulk_ctas", ctypes.c_int32),
         ("block", ctypes.c_int32),
         ("window_blocks", ctypes.c_int32),

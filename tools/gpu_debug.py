@@ -25,6 +25,6 @@ for N in [10**5, 3 * 10**5, 10**6]:
         ms = plan.run()
         st = plan.stats()
         print(f"lorenz N={N} rep{rep} kernel={ms:.1f}ms steps/s={N/(ms*1e-3):.3e} FMA/s={3*N*N/(ms*1e-3):.3e} "
-              f"tiles={st['bulk_tiles']} wait={st['leader_wait_ns']/1e6:.1f}ms ctas={st['bulk_ctas']}", flush=True)
+              f"tiles={st['bulk_tiles']} wait={st["leader_wait_ns"]/1e6:.1f}ms thr={st["leader_throttle_ns"]/1e6:.1f}ms ctas={st['bulk_ctas']}", flush=True)
     print("  y_N", plan.last_state(), flush=True)
     plan.close()
