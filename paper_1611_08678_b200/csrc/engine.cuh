@@ -27,7 +27,10 @@ namespace fabm {
 constexpr int kB = 128;                 // history block (targets = sources per tile)
 constexpr int kL = 3;                   // stepper window, in blocks
 constexpr int kSlots = kL * kB;         // 384 helper slots (12 helper warps)
-constexpr int kG = 3;                   // newest terms added by the leader itself
+constexpr int kG = 5;                   // newest terms (k = m-G+1..m) added by the leader itself
+constexpr int kHelperWarps = 6;         // warps 1,2,3,5,6,7 (SMSPs 1-3)
+constexpr int kSlotsPerThread = kSlots / (kHelperWarps * 32);  // 2
+constexpr int kBatch = 2;               // publishes consumed per helper wake-up
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRing = 64;               // published (y, f) ring in smem
@@ -53,6 +56,7 @@ struct DevCtrl {
   unsigned long long leader_wait_ns;
   unsigned long long bulk_tiles;
   unsigned long long leader_throttle_ns;
+  unsigned long long prof[8];  // FABM_PROFILE builds: leader phase cycles
   int pad2[16];
 };
 
@@ -72,6 +76,7 @@ struct EngineParams {
   int nb;                  // ceil(N / B)
   int n_agents;            // bulk agents = 16 * (gridDim.x - 1)
   unsigned long long timeout_ns;
+  int debug;               // dev experiments: 1 = leader alone (results invalid)
 };
 
 __device__ __forceinline__ long long lo_of(long long m) {
@@ -94,13 +99,12 @@ __device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int
 // STEPPER CTA
 // ======================================================================
 struct StepperSmem {
-  double wb[kSlots];
-  double wa[kSlots];
-  double ringY[kRing][4];
-  double ringF[kRing][4];
-  double hP[kHR][4];
-  double hC[kHR][4];
+  double wb[kSlots + 2 * kG];   // b_j, a_j for j < kSlots (zero beyond)
+  double wa[kSlots + 2 * kG];
+  double ring[kRing][8];    // published step k: y_k at [0, d), f_k at [d, 2d)
+  double hbuf[kHR][8];      // handoff of step m: P part at [0, d), C part at [d, 2d)
   double bulk[2][kB][2][4];
+  double cfirst[2][kB];     // first-node coefficient of each staged step (c_m, or c_m - a_m)
   uint64_t bars[kNumBars];
   int hflag[kHR];
   int hprog[kWarps];       // last step processed by each helper warp
@@ -113,7 +117,7 @@ struct StepperSmem {
 __device__ __forceinline__ int slowest_consumer(StepperSmem& S) {
   int lo = ld_volatile_smem(&S.io_done);
 #pragma unroll
-  for (int w = 1; w < kWarps; ++w) {
+  for (int w = 1; w < 8; ++w) {
     if ((w & 3) == 0) continue;
     const int p = ld_volatile_smem(&S.hprog[w]) + 1;
     lo = p < lo ? p : lo;
@@ -142,206 +146,408 @@ __device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperS
   return true;
 }
 
+// 2d doubles as d/2-ish 16-byte vectors (2d is even for every d)
+template <int D>
+__device__ __forceinline__ void st_pairs(double* dst, const double* v) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) reinterpret_cast<double2*>(dst)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+template <int D>
+__device__ __forceinline__ void ld_pairs(const double* src, double* v) {
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const double2 t = reinterpret_cast<const double2*>(src)[i];
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
+  }
+}
+
+// x*0 is +-0 for finite x and NaN otherwise: one NaN test covers a vector,
+// exactly (no overflow false positives), without a branch per value
+template <int D>
+__device__ __forceinline__ bool any_nonfinite(const double* v) {
+  double t = v[0] * 0.0;
+#pragma unroll
+  for (int i = 1; i < D; ++i) t = fma(v[i], 0.0, t);
+  return t != t;
+}
+
+struct LeaderCoef {
+  double b[kG], a[kG];  // b_0..b_{G-1}, a_0..a_{G-1}
+};
+
+template <int D>
+struct LeaderState {
+  double y0[D], fc[D], preP[D], preC[D];
+  double fh[kG - 2][D];  // f_{n-1}, f_{n-2}, ..., f_{n-G+2}
+  int err_kind;
+  long long err_step;
+#ifdef FABM_PROFILE
+  long long pc[6];
+  long long tp;
+#endif
+};
+
+#ifdef FABM_PROFILE
+#define LPROF(st, i) { const long long _t = clock64(); (st).pc[i] += _t - (st).tp; (st).tp = _t; }
+#else
+#define LPROF(st, i)
+#endif
+
+// One step n of the sequential chain (serial.py:150-170).  preP/preC hold
+// everything of step n except its f_n terms; the pre-sums of step n+1 are
+// formed from the (speculatively read) handoff H[n+1] in the shadow of the
+// chain.  Non-finite rhs outputs are recorded branch-free (first one wins);
+// the caller acts on them at block boundaries.  GENERIC handles n < 8 where
+// some history terms do not exist yet.
+template <int SYS, int D, bool GENERIC>
+__device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, const LeaderCoef& w,
+                                            LeaderState<D>& st, long long n, int slot1, int ring1,
+                                            unsigned long long& waited) {
+  const long long m1 = n + 1;
+  const int fl = ld_acquire_cta_smem(&S.hflag[slot1]);
+  double h1[2 * D];
+  ld_pairs<D>(&S.hbuf[slot1][0], h1);
+  // pre-sums of step m1: H[m1] + sum_{j=G-1..1} w_j f_{m1-j}, ascending k.
+  // f_{m1-j} for j >= 2 lives in st.fh[j-2]; f_{m1-1} = f_n = st.fc.
+  // Terms with k = m1-j < 0 (and k = 0 for the corrector) do not exist.
+  double cb[kG], ca[kG];
+#pragma unroll
+  for (int j = 1; j < kG; ++j) {
+    cb[j] = (!GENERIC || m1 - j >= 0) ? w.b[j] : 0.0;
+    ca[j] = (!GENERIC || m1 - j >= 1) ? w.a[j] : 0.0;
+  }
+  const double a0e = (!GENERIC || n >= 1) ? w.a[0] : 0.0;  // corrector interior starts at k = 1
+  double nP[D], nC[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    double p = h1[c], q = h1[D + c];
+#pragma unroll
+    for (int j = kG - 1; j >= 2; --j) {
+      p = fma(cb[j], st.fh[j - 2][c], p);
+      q = fma(ca[j], st.fh[j - 2][c], q);
+    }
+    nP[c] = fma(cb[1], st.fc[c], p);
+    nC[c] = fma(ca[1], st.fc[c], q);
+  }
+  const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
+  const double ha = P.ha;
+  double yP[D], fP[D], v[2 * D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(w.b[0], st.fc[c], st.preP[c]), ha), st.y0[c]);
+  Rhs<SYS, D>::eval(t1, yP, fP, P.params);
+#pragma unroll
+  for (int c = 0; c < D; ++c)  // ((c_n f0 + C_n) + fP/G2) * h^a + y0, serial.py:160-165
+    v[c] = add_rn(mul_rn(add_rn(fma(a0e, st.fc[c], st.preC[c]), mul_rn(P.ig, fP[c])), ha), st.y0[c]);
+  Rhs<SYS, D>::eval(t1, v, v + D, P.params);
+  // first non-finite rhs output: predictor before corrector (serial.py:157,167)
+  LPROF(st, 0)
+  const bool bp = any_nonfinite<D>(fP), bc = any_nonfinite<D>(v + D);
+  const int kind = bp ? KIND_PREDICTOR : (bc ? KIND_CORRECTOR : KIND_NONE);
+  const bool first = (kind != KIND_NONE) & (st.err_kind == KIND_NONE);
+  st.err_kind = first ? kind : st.err_kind;
+  st.err_step = first ? n : st.err_step;
+  // publish (y_{n+1}, f_{n+1})
+  st_pairs<D>(&S.ring[ring1][0], v);
+  mbar_arrive(&S.bars[ring1]);
+  LPROF(st, 1)
+  // slow path: the handoff of step n+1 was not ready when read
+  if (m1 < P.N && fl != static_cast<int>(m1) && P.debug == 0) {
+#ifdef FABM_PROFILE
+    st.pc[4] += 1;
+    const long long tw0 = clock64();
+#endif
+    if (!leader_wait_handoff(P, S, m1, waited)) return false;
+#ifdef FABM_PROFILE
+    st.pc[5] += clock64() - tw0;
+#endif
+    ld_pairs<D>(&S.hbuf[slot1][0], h1);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double p = h1[c], q = h1[D + c];
+#pragma unroll
+      for (int j = kG - 1; j >= 2; --j) {
+        p = fma(cb[j], st.fh[j - 2][c], p);
+        q = fma(ca[j], st.fh[j - 2][c], q);
+      }
+      nP[c] = fma(cb[1], st.fc[c], p);
+      nC[c] = fma(ca[1], st.fc[c], q);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    st.preP[c] = nP[c];
+    st.preC[c] = nC[c];
+#pragma unroll
+    for (int j = kG - 3; j >= 1; --j) st.fh[j][c] = st.fh[j - 1][c];
+    st.fh[0][c] = st.fc[c];
+    st.fc[c] = v[D + c];
+  }
+  LPROF(st, 2)
+  return true;
+}
+
+template <int D>
+__device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
+                                                   long long n_next, unsigned long long& throttled) {
+  if (st.err_kind != KIND_NONE) {
+    raise_abort(P, ERR_NONFINITE, st.err_kind, st.err_step, static_cast<double>(st.err_step + 1) * P.h);
+    st_volatile_smem(&S.abort, 1);
+    mbar_arrive(&S.bars[n_next % kNumBars]);
+    return false;
+  }
+  // ring back-pressure: the writer warp and every helper warp must have
+  // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
+  if (P.debug == 0 && n_next - slowest_consumer(S) > kRing - 24) {
+    unsigned spins = 0;
+    const unsigned long long w0 = global_ns();
+    while (n_next - slowest_consumer(S) > kRing - 24) {
+      if (((++spins) & 1023u) == 0) {
+        if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
+        if (global_ns() - w0 > P.timeout_ns) {
+          raise_abort(P, ERR_TIMEOUT, KIND_NONE, n_next, 0.0);
+          st_volatile_smem(&S.abort, 1);
+          return false;
+        }
+      }
+    }
+    throttled += global_ns() - w0;
+  }
+  return true;
+}
+#ifdef FABM_PROFILE
+#define LPROF_BLOCK(st) LPROF(st, 3)
+#else
+#define LPROF_BLOCK(st)
+#endif
+
 template <int SYS, int D>
 __device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
   const long long N = P.N;
-  const double h = P.h, ha = P.ha, ig = P.ig;
-  double y0[D], fm1[D], fc[D];
+  LeaderState<D> st;
+  double f0[D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) { y0[c] = P.y0[c]; fm1[c] = 0.0; }
-  Rhs<SYS, D>::eval(0.0, y0, fc, P.params);
-  const bool ok0 = all_finite<D>(fc);
+  for (int c = 0; c < D; ++c) {
+    st.y0[c] = P.y0[c];
 #pragma unroll
-  for (int c = 0; c < D; ++c) { S.ringY[0][c] = y0[c]; S.ringF[0][c] = fc[c]; }
-  if (!ok0) {
+    for (int j = 0; j < kG - 2; ++j) st.fh[j][c] = 0.0;
+  }
+  Rhs<SYS, D>::eval(0.0, st.y0, f0, P.params);
+  double v0[2 * D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) { v0[c] = st.y0[c]; v0[D + c] = f0[c]; st.fc[c] = f0[c]; }
+  st_pairs<D>(&S.ring[0][0], v0);
+  const bool bad0 = any_nonfinite<D>(f0);
+  if (bad0) {
     raise_abort(P, ERR_NONFINITE, KIND_INITIAL, 0, 0.0);
     st_volatile_smem(&S.abort, 1);
   }
   mbar_arrive(&S.bars[0]);
-  if (!ok0) return;
+  if (bad0) return;
 
-  const double b0 = P.wb[0], b1 = P.wb[1], b2 = P.wb[2];
-  const double a0 = P.wa[0], a1 = P.wa[1], a2 = P.wa[2];
+  LeaderCoef w;
+#pragma unroll
+  for (int j = 0; j < kG; ++j) { w.b[j] = P.wb[j]; w.a[j] = P.wa[j]; }
+  st.err_kind = KIND_NONE;
+  st.err_step = -1;
+#ifdef FABM_PROFILE
+  for (int i = 0; i < 6; ++i) st.pc[i] = 0;
+  st.tp = clock64();
+#endif
   unsigned long long waited = 0, throttled = 0;
 
-  // pre-sums of step n: everything but the f_n terms, i.e.
-  //   preP = (H_P[n] + b2 f_{n-2}) + b1 f_{n-1},  preC likewise with a (k >= 1)
-  // built one step ahead, off the critical path of the sequential chain.
-  double preP[D], preC[D];
-  if (!leader_wait_handoff(P, S, 0, waited)) return;
+  // pre-sums of step 0: the handoff H[0] (no f-terms yet)
+  if (P.debug == 0 && !leader_wait_handoff(P, S, 0, waited)) return;
+  {
+    double h0[2 * D];
+    ld_pairs<D>(&S.hbuf[0][0], h0);
 #pragma unroll
-  for (int c = 0; c < D; ++c) { preP[c] = S.hP[0][c]; preC[c] = S.hC[0][c]; }
-
-  for (long long n = 0; n < N; ++n) {
-    // ---- speculative read of the handoff of step n+1 (normally long ready);
-    // the data loads are issued after the flag load (in-order smem pipe)
-    const long long m1 = n + 1;
-    const int slot1 = static_cast<int>(m1 % kHR);
-    const int fl = ld_acquire_cta_smem(&S.hflag[slot1]);
-    double hp1[D], hc1[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) { hp1[c] = S.hP[slot1][c]; hc1[c] = S.hC[slot1][c]; }
-    // coefficients of step m1 for its f_{m1-2} = f_{n-1} and f_{m1-1} = f_n terms
-    const double nb2 = m1 >= 2 ? b2 : 0.0;
-    const double na2 = m1 >= 3 ? a2 : 0.0, na1 = m1 >= 2 ? a1 : 0.0;
-    double nP[D], nC[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      nP[c] = fma(b1, fc[c], fma(nb2, fm1[c], hp1[c]));
-      nC[c] = fma(na1, fc[c], fma(na2, fm1[c], hc1[c]));
-    }
-
-    // ---- the sequential chain of step n
-    const double t1 = static_cast<double>(n + 1) * h;  // (n + 1) * h, serial.py:151
-    const double a0e = n >= 1 ? a0 : 0.0;               // corrector interior starts at k = 1
-    double yP[D], fP[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(b0, fc[c], preP[c]), ha), y0[c]);  // serial.py:153-155
-    Rhs<SYS, D>::eval(t1, yP, fP, P.params);
-    if (!all_finite<D>(fP)) {
-      raise_abort(P, ERR_NONFINITE, KIND_PREDICTOR, n, t1);
-      st_volatile_smem(&S.abort, 1);
-      mbar_arrive(&S.bars[(n + 1) % kNumBars]);
-      break;
-    }
-    double y1[D], f1[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c)  // ((c_n f0 + C_n) + fP/G2) * h^a + y0, serial.py:160-165
-      y1[c] = add_rn(mul_rn(add_rn(fma(a0e, fc[c], preC[c]), mul_rn(ig, fP[c])), ha), y0[c]);
-    Rhs<SYS, D>::eval(t1, y1, f1, P.params);
-    if (!all_finite<D>(f1)) {
-      raise_abort(P, ERR_NONFINITE, KIND_CORRECTOR, n, t1);
-      st_volatile_smem(&S.abort, 1);
-      mbar_arrive(&S.bars[(n + 1) % kNumBars]);
-      break;
-    }
-    // ---- publish (y_{n+1}, f_{n+1})
-    const int ri = static_cast<int>((n + 1) % kRing);
-#pragma unroll
-    for (int c = 0; c < D; ++c) { S.ringY[ri][c] = y1[c]; S.ringF[ri][c] = f1[c]; }
-    mbar_arrive(&S.bars[(n + 1) % kNumBars]);
-
-    // ---- slow path: the handoff of step n+1 was not ready when read
-    if (m1 < N && fl != static_cast<int>(m1)) {
-      if (!leader_wait_handoff(P, S, m1, waited)) return;
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        nP[c] = fma(b1, fc[c], fma(nb2, fm1[c], S.hP[slot1][c]));
-        nC[c] = fma(na1, fc[c], fma(na2, fm1[c], S.hC[slot1][c]));
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < D; ++c) { preP[c] = nP[c]; preC[c] = nC[c]; fm1[c] = fc[c]; fc[c] = f1[c]; }
-
-    // ring back-pressure: the I/O warp and every helper warp must have
-    // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
-    if (((n + 1) & 7) == 0 && (n + 1) - slowest_consumer(S) > kRing - 24) {
-      unsigned spins = 0;
-      const unsigned long long w0 = global_ns();
-      while ((n + 1) - slowest_consumer(S) > kRing - 24) {
-        if (((++spins) & 1023u) == 0) {
-          if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return;
-          if (global_ns() - w0 > P.timeout_ns) {
-            raise_abort(P, ERR_TIMEOUT, KIND_NONE, n, 0.0);
-            st_volatile_smem(&S.abort, 1);
-            return;
-          }
-        }
-      }
-      throttled += global_ns() - w0;
-    }
+    for (int c = 0; c < D; ++c) { st.preP[c] = h0[c]; st.preC[c] = h0[D + c]; }
   }
+  long long n = 0;
+  // prologue: n < 8, where the f_{n-1}, f_{n-2} terms may not exist
+  for (; n < N && n < 8; ++n) {
+    if (!leader_step<SYS, D, true>(P, S, w, st, n, static_cast<int>((n + 1) % kHR),
+                                   static_cast<int>((n + 1) % kRing), waited))
+      return;
+  }
+  if (!leader_check_block<D>(P, S, st, n, throttled)) return;
+  // main loop: blocks of 8 steps, compile-time handoff slots, one check per block
+  while (n + 8 <= N) {
+    const int rbase = static_cast<int>(n % kRing);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (!leader_step<SYS, D, false>(P, S, w, st, n + u, (u + 1) % kHR, (rbase + u + 1) % kRing, waited))
+        return;
+    }
+    n += 8;
+    if (!leader_check_block<D>(P, S, st, n, throttled)) return;
+    LPROF_BLOCK(st)
+  }
+  for (; n < N; ++n) {
+    if (!leader_step<SYS, D, true>(P, S, w, st, n, static_cast<int>((n + 1) % kHR),
+                                   static_cast<int>((n + 1) % kRing), waited))
+      return;
+  }
+  if (!leader_check_block<D>(P, S, st, n, throttled)) return;
+#ifdef FABM_PROFILE
+  for (int i = 0; i < 4; ++i) P.ctrl->prof[i] = st.pc[i];
+  P.ctrl->prof[6] = st.pc[4];
+  P.ctrl->prof[3] = st.pc[5];
+#endif
   P.ctrl->leader_wait_ns = waited;
   P.ctrl->leader_throttle_ns = throttled;
 }
 
+// Helper thread: owns kSlotsPerThread future steps ("slots") m and pushes
+// every published f_k with k in [lo(m), m-G] into them, in ascending k; after
+// f_{m-G} it adds the staged bulk sum and the first-node term and hands the
+// slot to the leader, then re-opens it for step m + kSlots.  Wakes once per
+// kBatch publishes (acquire on the mbarrier of the newest one).  The push is
+// branch-free (a weight of 0 outside the window); only handoffs branch.
 template <int D>
-__device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid) {
-  const long long N = P.N;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  long long m = hid;
-  double accP[D], accC[D], f0[D];
-#pragma unroll
-  for (int c = 0; c < D; ++c) { accP[c] = 0.0; accC[c] = 0.0; f0[c] = 0.0; }
-  long long lo = lo_of(m);
-  long long kh = m - kG > 0 ? m - kG : 0;
-  double cm = m < N ? P.wc[m] : 0.0, am = m < N ? P.wa[m] : 0.0;
-
-  for (long long k = 0; k <= N; ++k) {
-    // wait for publication of step k
-    uint64_t* bar = &S.bars[k % kNumBars];
-    const uint32_t par = static_cast<uint32_t>((k / kNumBars) & 1);
-    unsigned spins = 0;
-    const unsigned long long w0 = global_ns();
-    while (!mbar_try(bar, par)) {
-      if (ld_volatile_smem(&S.abort)) return;
-      if (((++spins) & 255u) == 0) {
-        if (*((volatile int*)&P.ctrl->abort)) return;
-        if (global_ns() - w0 > P.timeout_ns) return;
+__device__ __forceinline__ bool helper_handoff(const EngineParams& P, StepperSmem& S, int m, const double* f0,
+                                               const double* accP, const double* accC) {
+  // the publisher staged block J: its first-node coefficients and, for
+  // J >= L, the bulk sums of the sources below lo (which include k = 0 in
+  // the a-sum, hence the coefficient c_m - a_m there)
+  const int J = m / kB;
+  if (ld_acquire_cta_smem(&S.bulk_flag) < J) {
+    unsigned sp2 = 0;
+    const unsigned long long w1 = global_ns();
+    while (ld_acquire_cta_smem(&S.bulk_flag) < J) {
+      if (ld_volatile_smem(&S.abort)) return false;
+      if (((++sp2) & 255u) == 0) {
+        if (*((volatile int*)&P.ctrl->abort)) return false;
+        if (global_ns() - w1 > P.timeout_ns) return false;
       }
     }
-    const int ri = static_cast<int>(k % kRing);
-    double fk[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) fk[c] = S.ringF[ri][c];
-    if (k == 0) {
-#pragma unroll
-      for (int c = 0; c < D; ++c) f0[c] = fk[c];
-    }
-    if (m < N && k >= lo && k <= m - kG) {
-      const int j = static_cast<int>(m - k);
-      const double wb = S.wb[j];
-      const double wa = k >= 1 ? S.wa[j] : 0.0;  // corrector interior excludes k = 0
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        accP[c] = fma(wb, fk[c], accP[c]);
-        accC[c] = fma(wa, fk[c], accC[c]);
-      }
-    }
-    if (m < N && k == kh) {
-      const long long J = m / kB;
-      double hp[D], hc[D];
-      if (J >= kL) {
-        // bulk sums (sources < lo) include k = 0 in the a-sum: fold (c_m - a_m) f0
-        unsigned sp2 = 0;
-        const unsigned long long w1 = global_ns();
-        while (ld_acquire_cta_smem(&S.bulk_flag) < static_cast<int>(J)) {
-          if (ld_volatile_smem(&S.abort)) return;
-          if (((++sp2) & 255u) == 0) {
-            if (*((volatile int*)&P.ctrl->abort)) return;
-            if (global_ns() - w1 > P.timeout_ns) return;
-          }
-        }
-        const int bsel = static_cast<int>(J & 1);
-        const int r = static_cast<int>(m % kB);
-        const double cma = cm - am;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          hp[c] = accP[c] + S.bulk[bsel][r][0][c];
-          hc[c] = add_rn(accC[c] + S.bulk[bsel][r][1][c], mul_rn(cma, f0[c]));
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          hp[c] = accP[c];
-          hc[c] = add_rn(accC[c], mul_rn(cm, f0[c]));
-        }
-      }
-      const int slot = static_cast<int>(m % kHR);
-#pragma unroll
-      for (int c = 0; c < D; ++c) { S.hP[slot][c] = hp[c]; S.hC[slot][c] = hc[c]; }
-      st_release_cta_smem(&S.hflag[slot], static_cast<int>(m));
-      // reopen the slot for step m + kSlots
-      m += kSlots;
-#pragma unroll
-      for (int c = 0; c < D; ++c) { accP[c] = 0.0; accC[c] = 0.0; }
-      lo = lo_of(m);
-      kh = m - kG;
-      if (m < N) { cm = P.wc[m]; am = P.wa[m]; }
-    }
-    __syncwarp();
-    if (lane == 0) st_volatile_smem(&S.hprog[warp], static_cast<int>(k));
   }
+  const int bsel = J & 1;
+  const int r = m % kB;
+  const double cf = S.cfirst[bsel][r];
+  double hv[2 * D];
+  if (J >= kL) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      hv[c] = accP[c] + S.bulk[bsel][r][0][c];
+      hv[D + c] = add_rn(accC[c] + S.bulk[bsel][r][1][c], mul_rn(cf, f0[c]));
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      hv[c] = accP[c];
+      hv[D + c] = add_rn(accC[c], mul_rn(cf, f0[c]));
+    }
+  }
+  const int slot = m % kHR;
+  st_pairs<D>(&S.hbuf[slot][0], hv);
+  st_release_cta_smem(&S.hflag[slot], m);
+  return true;
+}
+
+template <int D, bool FIRST>
+__device__ __forceinline__ bool helper_consume(const EngineParams& P, StepperSmem& S, int k, int N,
+                                               int (&m)[kSlotsPerThread], int (&lo)[kSlotsPerThread],
+                                               double (&accP)[kSlotsPerThread][D],
+                                               double (&accC)[kSlotsPerThread][D], double* f0) {
+  // f_k from the ring (the f half of the packed (y, f) row)
+  double fk[D];
+  const double* row = &S.ring[k % kRing][0];
+#pragma unroll
+  for (int c = 0; c < D; ++c) fk[c] = row[D + c];
+  if (FIRST) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) f0[c] = fk[c];
+  }
+#pragma unroll
+  for (int s = 0; s < kSlotsPerThread; ++s) {
+    const int j = m[s] - k;
+    const bool in = (k >= lo[s]) & (j >= kG);
+    const int jj = in ? j : 0;
+    const double wb = in ? S.wb[jj] : 0.0;
+    const double wa = (in && !FIRST) ? S.wa[jj] : 0.0;  // corrector interior excludes k = 0
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      accP[s][c] = fma(wb, fk[c], accP[s][c]);
+      accC[s][c] = fma(wa, fk[c], accC[s][c]);
+    }
+    // slots m <= G hand off after f_0; every other slot after f_{m-G}
+    const bool due = FIRST ? (m[s] <= kG) : (j == kG);
+    if (due && m[s] < N) {
+      if (!helper_handoff<D>(P, S, m[s], f0, accP[s], accC[s])) return false;
+      m[s] += kSlots;
+      lo[s] = static_cast<int>(lo_of(m[s]));
+#pragma unroll
+      for (int c = 0; c < D; ++c) { accP[s][c] = 0.0; accC[s][c] = 0.0; }
+    }
+  }
+  return true;
+}
+
+template <int D>
+__device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, int hwarp) {
+  constexpr int NS = kSlotsPerThread;
+  const int N = static_cast<int>(P.N);
+  const int lane = threadIdx.x & 31;
+  int m[NS], lo[NS];
+  double accP[NS][D], accC[NS][D], f0[D];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    m[s] = hid + s * (kSlots / NS);
+    lo[s] = static_cast<int>(lo_of(m[s]));
+#pragma unroll
+    for (int c = 0; c < D; ++c) { accP[s][c] = 0.0; accC[s][c] = 0.0; }
+  }
+#pragma unroll
+  for (int c = 0; c < D; ++c) f0[c] = 0.0;
+#ifdef FABM_PROFILE
+  long long hw_wait = 0, hw_work = 0, hw_batches = 0, hw_t = clock64();
+#endif
+
+  // batches [0], [1, kBatch], [kBatch+1, 2 kBatch], ...: step 0 alone, since
+  // the handoffs of steps 0..G need only f_0 and the leader waits for them
+  for (int k0 = 0, kl = 0; k0 <= N; k0 = kl + 1, kl = (k0 + kBatch - 1 < N) ? k0 + kBatch - 1 : N) {
+    uint64_t* bar = &S.bars[kl % kNumBars];
+    const uint32_t par = static_cast<uint32_t>((kl / kNumBars) & 1);
+    if (!mbar_test(bar, par)) {
+      unsigned spins = 0;
+      const unsigned long long w0 = global_ns();
+      while (!mbar_wait_hint(bar, par, 100000u)) {
+        if (ld_volatile_smem(&S.abort)) return;
+        if (((++spins) & 255u) == 0) {
+          if (*((volatile int*)&P.ctrl->abort)) return;
+          if (global_ns() - w0 > P.timeout_ns) return;
+        }
+      }
+    }
+#ifdef FABM_PROFILE
+    { const long long t = clock64(); hw_wait += t - hw_t; hw_t = t; ++hw_batches; }
+#endif
+    if (k0 == 0) {
+      if (!helper_consume<D, true>(P, S, 0, N, m, lo, accP, accC, f0)) return;
+    } else {
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int k = k0 + i;
+        if (k <= kl && !helper_consume<D, false>(P, S, k, N, m, lo, accP, accC, f0)) return;
+      }
+    }
+    if ((kl & 7) == 0 || kl == N) {
+      __syncwarp();
+      if (lane == 0) st_volatile_smem(&S.hprog[hwarp], kl);
+    }
+#ifdef FABM_PROFILE
+    { const long long t = clock64(); hw_work += t - hw_t; hw_t = t; }
+#endif
+  }
+#ifdef FABM_PROFILE
+  if (hid == 0) {
+    P.ctrl->prof[4] = hw_wait;
+    P.ctrl->prof[5] = hw_work;
+    P.ctrl->prof[7] = hw_batches;
+  }
+#endif
 }
 
 // Writer warp: streams published (y, f) from the smem ring to HBM in batches
@@ -358,7 +564,7 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
     const uint32_t par = static_cast<uint32_t>((kend / kNumBars) & 1);
     unsigned spins = 0;
     const unsigned long long w0 = global_ns();
-    while (!mbar_try(bar, par)) {
+    while (!mbar_wait_hint(bar, par, 100000u)) {
       if (ld_volatile_smem(&S.abort)) return;
       if (((++spins) & 255u) == 0) {
         if (*((volatile int*)&P.ctrl->abort)) return;
@@ -372,10 +578,12 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
     const long long k = k0 + lane;
     if (k <= kend) {
       const int ri = static_cast<int>(k % kRing);
+      double yf[2 * D];
+      ld_pairs<D>(&S.ring[ri][0], yf);
       double* yd = P.Y + k * D;
       double* fd = P.F + k * DS;
 #pragma unroll
-      for (int c = 0; c < D; ++c) { yd[c] = S.ringY[ri][c]; fd[c] = S.ringF[ri][c]; }
+      for (int c = 0; c < D; ++c) { yd[c] = yf[c]; fd[c] = yf[D + c]; }
     }
     __syncwarp();
     if (lane == 0) {
@@ -396,7 +604,7 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
   const int nb = P.nb;
   const int last_block = static_cast<int>(P.N / kB);  // complete source blocks at the end
   int published = 0;
-  int next_stage = kL;
+  int next_stage = 0;
   unsigned long long last_progress = global_ns();
   while (published < last_block || next_stage < nb) {
     bool progress = false;
@@ -412,20 +620,32 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
       published = io_block;
       progress = true;
     }
-    // (2) stage target block J once the helpers are done with buffer J&1
-    // (the leader has published step (J-1)*B) and the agents flagged it
+    // (2) stage block J once the helpers are done with buffer J&1 (the leader
+    // has published step (J-1)*B): first-node coefficients for every block,
+    // plus, for J >= L, the bulk sums once the agents flagged them complete
     if (next_stage < nb && ld_volatile_smem(&S.io_done) - 1 >= static_cast<long long>(next_stage - 1) * kB) {
-      int rdy = 0;
-      if (lane == 0) rdy = ld_acquire_gpu(&P.ready[next_stage]);
-      rdy = __shfl_sync(0xffffffffu, rdy, 0);
+      int rdy = 1;
+      if (next_stage >= kL) {
+        if (lane == 0) rdy = ld_acquire_gpu(&P.ready[next_stage]);
+        rdy = __shfl_sync(0xffffffffu, rdy, 0);
+      }
       if (rdy) {
         __syncwarp();
         const int J = next_stage;
-        const double* src = P.BK + static_cast<long long>(J) * kB * 2 * DS;
-        double* dst = &S.bulk[J & 1][0][0][0];
-        for (int i = lane; i < kB * 2 * D; i += 32) {
-          const int row = i / (2 * D), rem = i % (2 * D), half = rem / D, c = rem % D;
-          dst[(row * 2 + half) * 4 + c] = __ldcg(src + (row * 2 + half) * DS + c);
+        const long long m0 = static_cast<long long>(J) * kB;
+        for (int r = lane; r < kB; r += 32) {
+          const long long mm = m0 + r;
+          double cf = 0.0;
+          if (mm < P.N) cf = J >= kL ? P.wc[mm] - P.wa[mm] : P.wc[mm];
+          S.cfirst[J & 1][r] = cf;
+        }
+        if (J >= kL) {
+          const double* src = P.BK + m0 * 2 * DS;
+          double* dst = &S.bulk[J & 1][0][0][0];
+          for (int i = lane; i < kB * 2 * D; i += 32) {
+            const int row = i / (2 * D), rem = i % (2 * D), half = rem / D, c = rem % D;
+            dst[(row * 2 + half) * 4 + c] = __ldcg(src + (row * 2 + half) * DS + c);
+          }
         }
         __syncwarp();
         if (lane == 0) st_release_cta_smem(&S.bulk_flag, J);
@@ -450,11 +670,14 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
 template <int SYS, int D>
 __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < kSlots; i += kThreads) { S.wb[i] = P.wb[i]; S.wa[i] = P.wa[i]; }
+  for (int i = tid; i < kSlots + 2 * kG; i += kThreads) {
+    S.wb[i] = i < kSlots ? P.wb[i] : 0.0;
+    S.wa[i] = i < kSlots ? P.wa[i] : 0.0;
+  }
   if (tid < kHR) S.hflag[tid] = -1;
   if (tid < kWarps) S.hprog[tid] = -1;
   if (tid == 0) {
-    S.bulk_flag = kL - 1;
+    S.bulk_flag = -1;
     S.io_done = 0;
     S.io_block = 0;
     S.abort = 0;
@@ -465,11 +688,12 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
     if (lane == 0) stepper_leader<SYS, D>(P, S);
     return;
   }
+  if (P.debug == 1) return;
   if (warp == 4) { stepper_writer<D>(P, S, lane); return; }
   if (warp == 8) { stepper_publisher<D>(P, S, lane); return; }
-  if ((warp & 3) == 0) return;  // share the leader's SMSP: keep it quiet
-  const int hid = (warp - (warp >> 2) - 1) * 32 + lane;
-  stepper_helper<D>(P, S, hid);
+  if ((warp & 3) == 0 || warp > 7) return;  // SMSP 0 stays with the leader
+  const int hw = warp - (warp >> 2) - 1;    // warps 1,2,3,5,6,7 -> 0..5
+  stepper_helper<D>(P, S, hw * 32 + lane, warp);
 }
 
 // ======================================================================
@@ -663,6 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P)
   if (blockIdx.x == 0) {
     stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
   } else {
+    if (P.debug == 1) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     AgentSmem* A = reinterpret_cast<AgentSmem*>(smem_raw) + warp;
     bulk_agent<D>(P, *A, (blockIdx.x - 1) * kWarps + warp, lane);

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/fabm.h"
@@ -140,6 +141,11 @@ EngineLaunch pick_engine(int sys, int dim) {
 int stride_of(int dim) { return dim == 1 ? 1 : (dim == 2 ? 2 : 4); }
 
 }  // namespace
+
+static unsigned long long g_last_prof[8];
+extern "C" void fabm_debug_prof(unsigned long long* out) {
+  for (int i = 0; i < 8; ++i) out[i] = g_last_prof[i];
+}
 
 struct fabm_plan {
   int device = 0;
@@ -348,6 +354,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   P.n_agents = p->bulk_ctas * kWarps;
   const double tmo = timeout_s > 0 ? timeout_s : 60.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  if (const char* dbg = getenv("FABM_DEBUG_MODE")) P.debug = atoi(dbg);
   const int grid = 1 + p->bulk_ctas;
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
   CUDA_TRY(p->launch(P, grid, p->stream));
@@ -363,6 +370,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   p->stats.bulk_tiles = static_cast<int64_t>(h.bulk_tiles);
   p->stats.leader_wait_ns = static_cast<int64_t>(h.leader_wait_ns);
   p->stats.leader_throttle_ns = static_cast<int64_t>(h.leader_throttle_ns);
+  for (int i = 0; i < 8; ++i) g_last_prof[i] = h.prof[i];
   if (h.err_code != ERR_OK) {
     if (status) {
       status->code = h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;
