@@ -26,16 +26,17 @@ namespace fabm {
 // ------------------------------------------------------------ geometry
 constexpr int kB = 128;                 // history block (targets = sources per tile)
 constexpr int kL = 3;                   // stepper window, in blocks
-constexpr int kSlots = kL * kB;         // 384 helper slots (12 helper warps)
-constexpr int kG = 5;                   // newest terms (k = m-G+1..m) added by the leader itself
+constexpr int kSlots = kL * kB;         // 384 far-window slots
+constexpr int kChunk = 32;              // near window: k in [32(c-1), m-1] for m in chunk c (leader warp)
+constexpr int kGFar = 2 * kChunk + 1;   // sizing of the zero-padded weight tables
 constexpr int kHelperWarps = 6;         // warps 1,2,3,5,6,7 (SMSPs 1-3)
 constexpr int kSlotsPerThread = kSlots / (kHelperWarps * 32);  // 2
-constexpr int kBatch = 2;               // publishes consumed per helper wake-up
+constexpr int kBatch = 8;               // publishes consumed per helper wake-up
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRing = 64;               // published (y, f) ring in smem
 constexpr int kNumBars = 64;            // publish mbarriers (step k -> bar k % 64)
-constexpr int kHR = 8;                  // handoff ring
+constexpr int kHR = 128;                // far handoff ring (handoffs run ~60 steps ahead)
 constexpr int kR = 4;                   // targets per lane in a bulk tile
 constexpr int kWCols = 2 * kB / 4 + 2;  // transposed weight row length (+2 pad)
 constexpr int kMaxOwn = 256;            // owned target blocks per agent
@@ -99,18 +100,21 @@ __device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int
 // STEPPER CTA
 // ======================================================================
 struct StepperSmem {
-  double wb[kSlots + 2 * kG];   // b_j, a_j for j < kSlots (zero beyond)
-  double wa[kSlots + 2 * kG];
+  double wb[kSlots + 2 * kGFar];   // b_j, a_j for j < kSlots (zero beyond)
+  double wa[kSlots + 2 * kGFar];
   double ring[kRing][8];    // published step k: y_k at [0, d), f_k at [d, 2d)
-  double hbuf[kHR][8];      // handoff of step m: P part at [0, d), C part at [d, 2d)
+  double hbuf[kHR][8];      // far handoff of step m: P part at [0, d), C part at [d, 2d)
+  double xfer[2][8];        // near pre-sum of the next step, owner lane -> leader warp
+  double tb[4 * kChunk];    // near weights, tb[j + 2*kChunk - 1] = b_j for j >= 1, 0 for j <= 0
+  double ta[4 * kChunk];
   double bulk[2][kB][2][4];
   double cfirst[2][kB];     // first-node coefficient of each staged step (c_m, or c_m - a_m)
   uint64_t bars[kNumBars];
   int hflag[kHR];
-  int hprog[kWarps];       // last step processed by each helper warp
-  int bulk_flag;           // highest staged target block
-  int io_done;             // steps written to HBM by the writer warp
-  int io_block;            // complete source blocks written by the writer warp
+  int hprog[kWarps];        // last step processed by each helper warp
+  int bulk_flag;            // highest staged block
+  int io_done;              // steps written to HBM by the writer warp
+  int io_block;             // complete source blocks written by the writer warp
   int abort;
 };
 
@@ -125,7 +129,7 @@ __device__ __forceinline__ int slowest_consumer(StepperSmem& S) {
   return lo;
 }
 
-// spin until the helpers handed off step m (flag == m); false on abort/timeout
+// spin until the helpers handed off the far part of step m; false on abort/timeout
 __device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperSmem& S, long long m,
                                                  unsigned long long& waited) {
   const int slot = static_cast<int>(m % kHR);
@@ -135,9 +139,8 @@ __device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperS
     if (((++spins) & 1023u) == 0) {
       if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
       if (global_ns() - w0 > P.timeout_ns) {
-        raise_abort(P, ERR_TIMEOUT, KIND_NONE, m, 0.0);
+        if ((threadIdx.x & 31) == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, m, 0.0);
         st_volatile_smem(&S.abort, 1);
-        mbar_arrive(&S.bars[(m + 1) % kNumBars]);
         return false;
       }
     }
@@ -146,7 +149,7 @@ __device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperS
   return true;
 }
 
-// 2d doubles as d/2-ish 16-byte vectors (2d is even for every d)
+// 2d doubles as d 16-byte vectors (2d is even for every d)
 template <int D>
 __device__ __forceinline__ void st_pairs(double* dst, const double* v) {
 #pragma unroll
@@ -172,140 +175,133 @@ __device__ __forceinline__ bool any_nonfinite(const double* v) {
   return t != t;
 }
 
-struct LeaderCoef {
-  double b[kG], a[kG];  // b_0..b_{G-1}, a_0..a_{G-1}
-};
-
+// ----------------------------------------------------------------------
+// Leader warp (warp 0).  All 32 lanes run the sequential chain redundantly
+// (bitwise identical values), so every lane holds f_{n+1} the moment it is
+// computed and no broadcast is needed.  Lane l also keeps the NEAR window of
+// two future steps m = l and m = l + 32 (mod 64): the terms w_{m-k} f_k for
+// k in [m-64, m-1], pushed as soon as f_k exists.  The far remainder
+// (bulk + far window + first-node term) arrives from the helper warps about
+// 60 steps ahead of need, so the chain never waits on them in steady state.
+// ----------------------------------------------------------------------
 template <int D>
 struct LeaderState {
   double y0[D], fc[D], preP[D], preC[D];
-  double fh[kG - 2][D];  // f_{n-1}, f_{n-2}, ..., f_{n-G+2}
+  // near sums (P | C) of this lane's step in the current chunk (A) and the
+  // next chunk (B): lane l owns steps 32c + l
+  double accA[2 * D], accB[2 * D];
+  int cA;                // chunk index of A
   int err_kind;
   long long err_step;
-#ifdef FABM_PROFILE
-  long long pc[6];
-  long long tp;
-#endif
 };
 
-#ifdef FABM_PROFILE
-#define LPROF(st, i) { const long long _t = clock64(); (st).pc[i] += _t - (st).tp; (st).tp = _t; }
-#else
-#define LPROF(st, i)
-#endif
-
-// One step n of the sequential chain (serial.py:150-170).  preP/preC hold
-// everything of step n except its f_n terms; the pre-sums of step n+1 are
-// formed from the (speculatively read) handoff H[n+1] in the shadow of the
-// chain.  Non-finite rhs outputs are recorded branch-free (first one wins);
-// the caller acts on them at block boundaries.  GENERIC handles n < 8 where
-// some history terms do not exist yet.
-template <int SYS, int D, bool GENERIC>
-__device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, const LeaderCoef& w,
-                                            LeaderState<D>& st, long long n, int slot1, int ring1,
-                                            unsigned long long& waited) {
-  const long long m1 = n + 1;
-  const int fl = ld_acquire_cta_smem(&S.hflag[slot1]);
-  double h1[2 * D];
-  ld_pairs<D>(&S.hbuf[slot1][0], h1);
-  // pre-sums of step m1: H[m1] + sum_{j=G-1..1} w_j f_{m1-j}, ascending k.
-  // f_{m1-j} for j >= 2 lives in st.fh[j-2]; f_{m1-1} = f_n = st.fc.
-  // Terms with k = m1-j < 0 (and k = 0 for the corrector) do not exist.
-  double cb[kG], ca[kG];
+// near sums of step m1 (owner lane -> all lanes via smem) and its far handoff
+template <int D>
+__device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st, long long m1, int lane,
+                                             double* nr, double* fr) {
+  if ((m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation A <- B, B <- 0
 #pragma unroll
-  for (int j = 1; j < kG; ++j) {
-    cb[j] = (!GENERIC || m1 - j >= 0) ? w.b[j] : 0.0;
-    ca[j] = (!GENERIC || m1 - j >= 1) ? w.a[j] : 0.0;
+    for (int c = 0; c < 2 * D; ++c) { st.accA[c] = st.accB[c]; st.accB[c] = 0.0; }
+    st.cA += 1;
   }
-  const double a0e = (!GENERIC || n >= 1) ? w.a[0] : 0.0;  // corrector interior starts at k = 1
-  double nP[D], nC[D];
+  const int owner = static_cast<int>(m1 & (kChunk - 1));
+  double* xb = &S.xfer[m1 & 1][0];
+  if (lane == owner) st_pairs<D>(xb, st.accA);
+  __syncwarp();
+  const int slot = static_cast<int>(m1 % kHR);
+  const int fl = ld_acquire_cta_smem(&S.hflag[slot]);
+  ld_pairs<D>(xb, nr);
+  ld_pairs<D>(&S.hbuf[slot][0], fr);
+  return fl;
+}
+
+// push f_k (k = m1, just computed) into the near sums of A and B; the padded
+// weight tables give 0 for steps already consumed (j <= 0)
+template <int D, bool K0>
+__device__ __forceinline__ void leader_push(const StepperSmem& S, LeaderState<D>& st, long long m1, int lane,
+                                            const double* fk) {
+  const int k = static_cast<int>(m1);
+  const int jA = st.cA * kChunk + lane - k;  // -31..31
+  const int jB = jA + kChunk;                // 1..63
+  const double wbA = S.tb[jA + 2 * kChunk - 1], wbB = S.tb[jB + 2 * kChunk - 1];
+  const double waA = K0 ? 0.0 : S.ta[jA + 2 * kChunk - 1];  // corrector interior excludes k = 0
+  const double waB = K0 ? 0.0 : S.ta[jB + 2 * kChunk - 1];
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    double p = h1[c], q = h1[D + c];
-#pragma unroll
-    for (int j = kG - 1; j >= 2; --j) {
-      p = fma(cb[j], st.fh[j - 2][c], p);
-      q = fma(ca[j], st.fh[j - 2][c], q);
-    }
-    nP[c] = fma(cb[1], st.fc[c], p);
-    nC[c] = fma(ca[1], st.fc[c], q);
+    st.accA[c] = fma(wbA, fk[c], st.accA[c]);
+    st.accA[D + c] = fma(waA, fk[c], st.accA[D + c]);
+    st.accB[c] = fma(wbB, fk[c], st.accB[c]);
+    st.accB[D + c] = fma(waB, fk[c], st.accB[D + c]);
   }
+}
+
+// One step n of the sequential chain (serial.py:150-170).
+template <int SYS, int D>
+__device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, LeaderState<D>& st,
+                                            double b0, double a0, long long n, int lane,
+                                            unsigned long long& waited) {
+  const long long m1 = n + 1;
+  double nr[2 * D], fr[2 * D];
+  const int fl = leader_gather<D>(S, st, m1, lane, nr, fr);
   const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
   const double ha = P.ha;
+  const double a0e = n >= 1 ? a0 : 0.0;  // corrector interior starts at k = 1
   double yP[D], fP[D], v[2 * D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(w.b[0], st.fc[c], st.preP[c]), ha), st.y0[c]);
+  for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(b0, st.fc[c], st.preP[c]), ha), st.y0[c]);
   Rhs<SYS, D>::eval(t1, yP, fP, P.params);
 #pragma unroll
   for (int c = 0; c < D; ++c)  // ((c_n f0 + C_n) + fP/G2) * h^a + y0, serial.py:160-165
     v[c] = add_rn(mul_rn(add_rn(fma(a0e, st.fc[c], st.preC[c]), mul_rn(P.ig, fP[c])), ha), st.y0[c]);
   Rhs<SYS, D>::eval(t1, v, v + D, P.params);
   // first non-finite rhs output: predictor before corrector (serial.py:157,167)
-  LPROF(st, 0)
   const bool bp = any_nonfinite<D>(fP), bc = any_nonfinite<D>(v + D);
   const int kind = bp ? KIND_PREDICTOR : (bc ? KIND_CORRECTOR : KIND_NONE);
   const bool first = (kind != KIND_NONE) & (st.err_kind == KIND_NONE);
   st.err_kind = first ? kind : st.err_kind;
   st.err_step = first ? n : st.err_step;
   // publish (y_{n+1}, f_{n+1})
-  st_pairs<D>(&S.ring[ring1][0], v);
-  mbar_arrive(&S.bars[ring1]);
-  LPROF(st, 1)
-  // slow path: the handoff of step n+1 was not ready when read
-  if (m1 < P.N && fl != static_cast<int>(m1) && P.debug == 0) {
-#ifdef FABM_PROFILE
-    st.pc[4] += 1;
-    const long long tw0 = clock64();
-#endif
-    if (!leader_wait_handoff(P, S, m1, waited)) return false;
-#ifdef FABM_PROFILE
-    st.pc[5] += clock64() - tw0;
-#endif
-    ld_pairs<D>(&S.hbuf[slot1][0], h1);
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      double p = h1[c], q = h1[D + c];
-#pragma unroll
-      for (int j = kG - 1; j >= 2; --j) {
-        p = fma(cb[j], st.fh[j - 2][c], p);
-        q = fma(ca[j], st.fh[j - 2][c], q);
-      }
-      nP[c] = fma(cb[1], st.fc[c], p);
-      nC[c] = fma(ca[1], st.fc[c], q);
-    }
+  const int ri = static_cast<int>(m1 % kRing);
+  if (lane == 0) {
+    st_pairs<D>(&S.ring[ri][0], v);
+    mbar_arrive(&S.bars[ri]);
   }
+  leader_push<D, false>(S, st, m1, lane, v + D);
+  // slow path: the far handoff of step n+1 was not ready when read
+  if (m1 < P.N && fl != static_cast<int>(m1)) {
+    if (!leader_wait_handoff(P, S, m1, waited)) return false;
+    ld_pairs<D>(&S.hbuf[m1 % kHR][0], fr);
+  }
+  // pre-sums of step n+1 = near + far
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    st.preP[c] = nP[c];
-    st.preC[c] = nC[c];
-#pragma unroll
-    for (int j = kG - 3; j >= 1; --j) st.fh[j][c] = st.fh[j - 1][c];
-    st.fh[0][c] = st.fc[c];
+    st.preP[c] = nr[c] + fr[c];
+    st.preC[c] = nr[D + c] + fr[D + c];
     st.fc[c] = v[D + c];
   }
-  LPROF(st, 2)
   return true;
 }
 
 template <int D>
 __device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
-                                                   long long n_next, unsigned long long& throttled) {
+                                                   long long n_next, int lane, unsigned long long& throttled) {
   if (st.err_kind != KIND_NONE) {
-    raise_abort(P, ERR_NONFINITE, st.err_kind, st.err_step, static_cast<double>(st.err_step + 1) * P.h);
+    if (lane == 0)
+      raise_abort(P, ERR_NONFINITE, st.err_kind, st.err_step, static_cast<double>(st.err_step + 1) * P.h);
     st_volatile_smem(&S.abort, 1);
-    mbar_arrive(&S.bars[n_next % kNumBars]);
+    if (lane == 0) mbar_arrive(&S.bars[n_next % kNumBars]);
     return false;
   }
   // ring back-pressure: the writer warp and every helper warp must have
   // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
-  if (P.debug == 0 && n_next - slowest_consumer(S) > kRing - 24) {
+  if (n_next - slowest_consumer(S) > kRing - 24) {
     unsigned spins = 0;
     const unsigned long long w0 = global_ns();
     while (n_next - slowest_consumer(S) > kRing - 24) {
       if (((++spins) & 1023u) == 0) {
         if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
         if (global_ns() - w0 > P.timeout_ns) {
-          raise_abort(P, ERR_TIMEOUT, KIND_NONE, n_next, 0.0);
+          if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, n_next, 0.0);
           st_volatile_smem(&S.abort, 1);
           return false;
         }
@@ -315,96 +311,76 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
   }
   return true;
 }
-#ifdef FABM_PROFILE
-#define LPROF_BLOCK(st) LPROF(st, 3)
-#else
-#define LPROF_BLOCK(st)
-#endif
 
 template <int SYS, int D>
-__device__ void stepper_leader(const EngineParams& P, StepperSmem& S) {
+__device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) {
   const long long N = P.N;
   LeaderState<D> st;
   double f0[D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) {
-    st.y0[c] = P.y0[c];
-#pragma unroll
-    for (int j = 0; j < kG - 2; ++j) st.fh[j][c] = 0.0;
-  }
+  for (int c = 0; c < D; ++c) st.y0[c] = P.y0[c];
   Rhs<SYS, D>::eval(0.0, st.y0, f0, P.params);
-  double v0[2 * D];
-#pragma unroll
-  for (int c = 0; c < D; ++c) { v0[c] = st.y0[c]; v0[D + c] = f0[c]; st.fc[c] = f0[c]; }
-  st_pairs<D>(&S.ring[0][0], v0);
   const bool bad0 = any_nonfinite<D>(f0);
-  if (bad0) {
-    raise_abort(P, ERR_NONFINITE, KIND_INITIAL, 0, 0.0);
-    st_volatile_smem(&S.abort, 1);
+  if (lane == 0) {
+    double v0[2 * D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) { v0[c] = st.y0[c]; v0[D + c] = f0[c]; }
+    st_pairs<D>(&S.ring[0][0], v0);
+    if (bad0) raise_abort(P, ERR_NONFINITE, KIND_INITIAL, 0, 0.0);
   }
-  mbar_arrive(&S.bars[0]);
+  if (bad0) st_volatile_smem(&S.abort, 1);
+  if (lane == 0) mbar_arrive(&S.bars[0]);
   if (bad0) return;
 
-  LeaderCoef w;
-#pragma unroll
-  for (int j = 0; j < kG; ++j) { w.b[j] = P.wb[j]; w.a[j] = P.wa[j]; }
+  const double b0 = P.wb[0], a0 = P.wa[0];
   st.err_kind = KIND_NONE;
   st.err_step = -1;
-#ifdef FABM_PROFILE
-  for (int i = 0; i < 6; ++i) st.pc[i] = 0;
-  st.tp = clock64();
-#endif
   unsigned long long waited = 0, throttled = 0;
+  st.cA = 0;
+#pragma unroll
+  for (int c = 0; c < 2 * D; ++c) { st.accA[c] = 0.0; st.accB[c] = 0.0; }
 
-  // pre-sums of step 0: the handoff H[0] (no f-terms yet)
-  if (P.debug == 0 && !leader_wait_handoff(P, S, 0, waited)) return;
+  // step 0: its pre-sums are the far handoff alone (c_0 f_0); then f_0 enters
+  // the near sums of steps 1..63
+  if (!leader_wait_handoff(P, S, 0, waited)) return;
   {
-    double h0[2 * D];
-    ld_pairs<D>(&S.hbuf[0][0], h0);
+    double nr[2 * D], fr[2 * D];
+    leader_gather<D>(S, st, 0, lane, nr, fr);
 #pragma unroll
-    for (int c = 0; c < D; ++c) { st.preP[c] = h0[c]; st.preC[c] = h0[D + c]; }
-  }
-  long long n = 0;
-  // prologue: n < 8, where the f_{n-1}, f_{n-2} terms may not exist
-  for (; n < N && n < 8; ++n) {
-    if (!leader_step<SYS, D, true>(P, S, w, st, n, static_cast<int>((n + 1) % kHR),
-                                   static_cast<int>((n + 1) % kRing), waited))
-      return;
-  }
-  if (!leader_check_block<D>(P, S, st, n, throttled)) return;
-  // main loop: blocks of 8 steps, compile-time handoff slots, one check per block
-  while (n + 8 <= N) {
-    const int rbase = static_cast<int>(n % kRing);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (!leader_step<SYS, D, false>(P, S, w, st, n + u, (u + 1) % kHR, (rbase + u + 1) % kRing, waited))
-        return;
+    for (int c = 0; c < D; ++c) {
+      st.preP[c] = nr[c] + fr[c];
+      st.preC[c] = nr[D + c] + fr[D + c];
     }
+  }
+  leader_push<D, true>(S, st, 0, lane, f0);
+#pragma unroll
+  for (int c = 0; c < D; ++c) st.fc[c] = f0[c];
+
+  long long n = 0;
+  while (n + 8 <= N) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (!leader_step<SYS, D>(P, S, st, b0, a0, n + u, lane, waited)) return;
     n += 8;
-    if (!leader_check_block<D>(P, S, st, n, throttled)) return;
-    LPROF_BLOCK(st)
+    if (!leader_check_block<D>(P, S, st, n, lane, throttled)) return;
   }
-  for (; n < N; ++n) {
-    if (!leader_step<SYS, D, true>(P, S, w, st, n, static_cast<int>((n + 1) % kHR),
-                                   static_cast<int>((n + 1) % kRing), waited))
-      return;
+  for (; n < N; ++n)
+    if (!leader_step<SYS, D>(P, S, st, b0, a0, n, lane, waited)) return;
+  if (!leader_check_block<D>(P, S, st, n, lane, throttled)) return;
+  if (lane == 0) {
+    P.ctrl->leader_wait_ns = waited;
+    P.ctrl->leader_throttle_ns = throttled;
   }
-  if (!leader_check_block<D>(P, S, st, n, throttled)) return;
-#ifdef FABM_PROFILE
-  for (int i = 0; i < 4; ++i) P.ctrl->prof[i] = st.pc[i];
-  P.ctrl->prof[6] = st.pc[4];
-  P.ctrl->prof[3] = st.pc[5];
-#endif
-  P.ctrl->leader_wait_ns = waited;
-  P.ctrl->leader_throttle_ns = throttled;
 }
 
-// Helper thread: owns kSlotsPerThread future steps ("slots") m and pushes
-// every published f_k with k in [lo(m), m-G] into them, in ascending k; after
-// f_{m-G} it adds the staged bulk sum and the first-node term and hands the
-// slot to the leader, then re-opens it for step m + kSlots.  Wakes once per
-// kBatch publishes (acquire on the mbarrier of the newest one).  The push is
-// branch-free (a weight of 0 outside the window); only handoffs branch.
+// ----------------------------------------------------------------------
+// Helper threads (warps 1,2,3,5,6,7): each owns kSlotsPerThread far slots m
+// and pushes every published f_k with k in [lo(m), m-65] into them, in
+// ascending k; after f_{m-65} it adds the staged bulk sum and the first-node
+// term and hands the far part to the leader warp (~60 steps before it is
+// needed), then re-opens the slot for step m + kSlots.  Wakes once per
+// kBatch publishes.  The push is branch-free; only handoffs branch.
+// ----------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ bool helper_handoff(const EngineParams& P, StepperSmem& S, int m, const double* f0,
                                                const double* accP, const double* accC) {
@@ -451,7 +427,6 @@ __device__ __forceinline__ bool helper_consume(const EngineParams& P, StepperSme
                                                int (&m)[kSlotsPerThread], int (&lo)[kSlotsPerThread],
                                                double (&accP)[kSlotsPerThread][D],
                                                double (&accC)[kSlotsPerThread][D], double* f0) {
-  // f_k from the ring (the f half of the packed (y, f) row)
   double fk[D];
   const double* row = &S.ring[k % kRing][0];
 #pragma unroll
@@ -463,7 +438,8 @@ __device__ __forceinline__ bool helper_consume(const EngineParams& P, StepperSme
 #pragma unroll
   for (int s = 0; s < kSlotsPerThread; ++s) {
     const int j = m[s] - k;
-    const bool in = (k >= lo[s]) & (j >= kG);
+    const int kh = (m[s] & ~(kChunk - 1)) - kChunk - 1;  // last far term: 32(c-1) - 1
+    const bool in = (k >= lo[s]) & (k <= kh);
     const int jj = in ? j : 0;
     const double wb = in ? S.wb[jj] : 0.0;
     const double wa = (in && !FIRST) ? S.wa[jj] : 0.0;  // corrector interior excludes k = 0
@@ -472,8 +448,8 @@ __device__ __forceinline__ bool helper_consume(const EngineParams& P, StepperSme
       accP[s][c] = fma(wb, fk[c], accP[s][c]);
       accC[s][c] = fma(wa, fk[c], accC[s][c]);
     }
-    // slots m <= G hand off after f_0; every other slot after f_{m-G}
-    const bool due = FIRST ? (m[s] <= kG) : (j == kG);
+    // slots of chunks 0 and 1 hand off after f_0; every other slot after f_kh
+    const bool due = FIRST ? (kh <= 0) : (k == kh);
     if (due && m[s] < N) {
       if (!helper_handoff<D>(P, S, m[s], f0, accP[s], accC[s])) return false;
       m[s] += kSlots;
@@ -501,12 +477,9 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
   }
 #pragma unroll
   for (int c = 0; c < D; ++c) f0[c] = 0.0;
-#ifdef FABM_PROFILE
-  long long hw_wait = 0, hw_work = 0, hw_batches = 0, hw_t = clock64();
-#endif
 
   // batches [0], [1, kBatch], [kBatch+1, 2 kBatch], ...: step 0 alone, since
-  // the handoffs of steps 0..G need only f_0 and the leader waits for them
+  // the handoffs of chunks 0 and 1 need only f_0 and the leader waits for them
   for (int k0 = 0, kl = 0; k0 <= N; k0 = kl + 1, kl = (k0 + kBatch - 1 < N) ? k0 + kBatch - 1 : N) {
     uint64_t* bar = &S.bars[kl % kNumBars];
     const uint32_t par = static_cast<uint32_t>((kl / kNumBars) & 1);
@@ -521,9 +494,6 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
         }
       }
     }
-#ifdef FABM_PROFILE
-    { const long long t = clock64(); hw_wait += t - hw_t; hw_t = t; ++hw_batches; }
-#endif
     if (k0 == 0) {
       if (!helper_consume<D, true>(P, S, 0, N, m, lo, accP, accC, f0)) return;
     } else {
@@ -533,21 +503,9 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
         if (k <= kl && !helper_consume<D, false>(P, S, k, N, m, lo, accP, accC, f0)) return;
       }
     }
-    if ((kl & 7) == 0 || kl == N) {
-      __syncwarp();
-      if (lane == 0) st_volatile_smem(&S.hprog[hwarp], kl);
-    }
-#ifdef FABM_PROFILE
-    { const long long t = clock64(); hw_work += t - hw_t; hw_t = t; }
-#endif
+    __syncwarp();
+    if (lane == 0) st_volatile_smem(&S.hprog[hwarp], kl);
   }
-#ifdef FABM_PROFILE
-  if (hid == 0) {
-    P.ctrl->prof[4] = hw_wait;
-    P.ctrl->prof[5] = hw_work;
-    P.ctrl->prof[7] = hw_batches;
-  }
-#endif
 }
 
 // Writer warp: streams published (y, f) from the smem ring to HBM in batches
@@ -670,11 +628,16 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
 template <int SYS, int D>
 __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < kSlots + 2 * kG; i += kThreads) {
+  for (int i = tid; i < kSlots + 2 * kGFar; i += kThreads) {
     S.wb[i] = i < kSlots ? P.wb[i] : 0.0;
     S.wa[i] = i < kSlots ? P.wa[i] : 0.0;
   }
-  if (tid < kHR) S.hflag[tid] = -1;
+  for (int i = tid; i < 4 * kChunk; i += kThreads) {
+    const int j = i - (2 * kChunk - 1);
+    S.tb[i] = (j >= 1 && j < kSlots) ? P.wb[j] : 0.0;
+    S.ta[i] = (j >= 1 && j < kSlots) ? P.wa[j] : 0.0;
+  }
+  for (int i = tid; i < kHR; i += kThreads) S.hflag[i] = -1;
   if (tid < kWarps) S.hprog[tid] = -1;
   if (tid == 0) {
     S.bulk_flag = -1;
@@ -684,14 +647,10 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
     for (int i = 0; i < kNumBars; ++i) mbar_init(&S.bars[i], 1);
   }
   __syncthreads();
-  if (warp == 0) {
-    if (lane == 0) stepper_leader<SYS, D>(P, S);
-    return;
-  }
-  if (P.debug == 1) return;
+  if (warp == 0) { stepper_leader<SYS, D>(P, S, lane); return; }
   if (warp == 4) { stepper_writer<D>(P, S, lane); return; }
   if (warp == 8) { stepper_publisher<D>(P, S, lane); return; }
-  if ((warp & 3) == 0 || warp > 7) return;  // SMSP 0 stays with the leader
+  if ((warp & 3) == 0 || warp > 7) return;  // SMSP 0 stays with the leader warp
   const int hw = warp - (warp >> 2) - 1;    // warps 1,2,3,5,6,7 -> 0..5
   stepper_helper<D>(P, S, hw * 32 + lane, warp);
 }
@@ -887,8 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P)
   if (blockIdx.x == 0) {
     stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
   } else {
-    if (P.debug == 1) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     AgentSmem* A = reinterpret_cast<AgentSmem*>(smem_raw) + warp;
     bulk_agent<D>(P, *A, (blockIdx.x - 1) * kWarps + warp, lane);
   }
