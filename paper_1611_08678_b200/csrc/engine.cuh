@@ -25,11 +25,11 @@ namespace fabm {
 
 // ------------------------------------------------------------ geometry
 constexpr int kB = 128;                 // history block (targets = sources per tile)
-constexpr int kL = 3;                   // stepper window, in blocks
-constexpr int kSlots = kL * kB;         // 384 far-window slots
+constexpr int kL = 4;                   // stepper window, in blocks (bulk slack: L-1 blocks)
+constexpr int kSlots = kL * kB;         // 512 far-window slots
 constexpr int kChunk = 32;              // near window: k in [32(c-1), m-1] for m in chunk c (leader warp)
 constexpr int kGFar = 2 * kChunk + 1;   // sizing of the zero-padded weight tables
-constexpr int kHelperWarps = 6;         // warps 1,2,3,5,6,7 (SMSPs 1-3)
+constexpr int kHelperWarps = 8;         // warps 1,2,3,5,6,7,9,10 (SMSPs 1-3)
 constexpr int kSlotsPerThread = kSlots / (kHelperWarps * 32);  // 2
 constexpr int kBatch = 8;               // publishes consumed per helper wake-up
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
@@ -77,6 +77,7 @@ struct EngineParams {
   int nb;                  // ceil(N / B)
   int n_agents;            // bulk agents = 16 * (gridDim.x - 1)
   unsigned long long timeout_ns;
+  unsigned long long* trace;  // FABM_PROFILE: per block {src published, ready, staged, first need}
   int debug;               // dev experiments: 1 = leader alone (results invalid)
 };
 
@@ -118,11 +119,13 @@ struct StepperSmem {
   int abort;
 };
 
+__device__ __forceinline__ int helper_index(int warp) { return warp - (warp >> 2) - 1; }
+
 __device__ __forceinline__ int slowest_consumer(StepperSmem& S) {
   int lo = ld_volatile_smem(&S.io_done);
 #pragma unroll
-  for (int w = 1; w < 8; ++w) {
-    if ((w & 3) == 0) continue;
+  for (int w = 1; w < kWarps; ++w) {
+    if ((w & 3) == 0 || helper_index(w) >= kHelperWarps) continue;
     const int p = ld_volatile_smem(&S.hprog[w]) + 1;
     lo = p < lo ? p : lo;
   }
@@ -388,6 +391,9 @@ __device__ __forceinline__ bool helper_handoff(const EngineParams& P, StepperSme
   // J >= L, the bulk sums of the sources below lo (which include k = 0 in
   // the a-sum, hence the coefficient c_m - a_m there)
   const int J = m / kB;
+#ifdef FABM_PROFILE
+  if (P.trace && (m % kB) == 0) P.trace[4 * J + 3] = global_ns();
+#endif
   if (ld_acquire_cta_smem(&S.bulk_flag) < J) {
     unsigned sp2 = 0;
     const unsigned long long w1 = global_ns();
@@ -574,6 +580,10 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
       if (lane == 0) {
         __threadfence();  // cumulative over the writer's rows (acquired above)
         st_release_gpu(&P.ctrl->src_done, io_block);
+#ifdef FABM_PROFILE
+        if (P.trace)
+          for (int q = published; q < io_block; ++q) P.trace[4 * q + 0] = global_ns();
+#endif
       }
       published = io_block;
       progress = true;
@@ -607,6 +617,9 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
         }
         __syncwarp();
         if (lane == 0) st_release_cta_smem(&S.bulk_flag, J);
+#ifdef FABM_PROFILE
+        if (P.trace && lane == 0) P.trace[4 * J + 2] = global_ns();
+#endif
         ++next_stage;
         progress = true;
       }
@@ -650,8 +663,9 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
   if (warp == 0) { stepper_leader<SYS, D>(P, S, lane); return; }
   if (warp == 4) { stepper_writer<D>(P, S, lane); return; }
   if (warp == 8) { stepper_publisher<D>(P, S, lane); return; }
-  if ((warp & 3) == 0 || warp > 7) return;  // SMSP 0 stays with the leader warp
-  const int hw = warp - (warp >> 2) - 1;    // warps 1,2,3,5,6,7 -> 0..5
+  if ((warp & 3) == 0) return;  // SMSP 0 stays with the leader warp
+  const int hw = helper_index(warp);  // warps 1,2,3,5,6,7,9,10 -> 0..7
+  if (hw >= kHelperWarps) return;
   stepper_helper<D>(P, S, hw * 32 + lane, warp);
 }
 
@@ -752,13 +766,22 @@ __device__ __forceinline__ void agent_tile(const EngineParams& P, AgentSmem& A, 
   }
 }
 
+// Round-robin ownership: agent a owns targets J = L + a + i*nA, so every
+// newly completed source block brings each agent about the same number of
+// tiles (one per owned target above it).
+__device__ __forceinline__ int owned_target(int agent, int i, int nA) { return kL + agent + i * nA; }
+__device__ __forceinline__ int owned_count(int agent, int nA, int n_targets) {
+  return agent < n_targets ? (n_targets - 1 - agent) / nA + 1 : 0;
+}
+
 template <int D>
 __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int lane) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
   if (agent >= n_targets) return;
   const int nA = P.n_agents;
-  const int nown = (n_targets - 1 - agent) / nA + 1;
+  const int nown = owned_count(agent, nA, n_targets);
+  if (nown == 0) return;
   for (int i = lane; i < nown; i += 32) A.own_next[i] = 0;
   __syncwarp();
   double accP[kR][D], accC[kR][D];
@@ -770,6 +793,12 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
   unsigned long long tiles = 0;
   unsigned long long last_progress = global_ns();
 
+#ifdef FABM_PROFILE
+  long long c_tile = 0, c_idle = 0, c_sw = 0, c_t = clock64();
+#define APROF(var) { const long long _t = clock64(); var += _t - c_t; c_t = _t; }
+#else
+#define APROF(var)
+#endif
   while (done < nown) {
     int M = 0, ab = 0;
     if (lane == 0) { M = ld_acquire_gpu(&P.ctrl->src_done); ab = ld_relaxed_gpu(&P.ctrl->abort); }
@@ -783,7 +812,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       const int i = b0 + lane;
       bool pend = false;
       if (i < nown) {
-        const int J = kL + agent + i * nA;
+        const int J = owned_target(agent, i, nA);
         const int nx = A.own_next[i];
         const int lim = min(M, J - kL + 1);
         pend = nx < lim;
@@ -793,6 +822,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     }
     if (best < 0) {
       __nanosleep(256);
+      APROF(c_idle)
       if (global_ns() - last_progress > P.timeout_ns) {
         if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, -1, 0.0);
         return;
@@ -800,9 +830,9 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       continue;
     }
     last_progress = global_ns();
-    const int J = kL + agent + best * nA;
+    const int J = owned_target(agent, best, nA);
     if (cur != best) {
-      if (cur >= 0) agent_store_acc<D>(P, kL + agent + cur * nA, lane, accP, accC);
+      if (cur >= 0) agent_store_acc<D>(P, owned_target(agent, cur, nA), lane, accP, accC);
       if (A.own_next[best] > 0) {
         agent_load_acc<D>(P, J, lane, accP, accC);
       } else {
@@ -813,6 +843,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       }
       cur = best;
     }
+    APROF(c_sw)
     const int lim = min(M, J - kL + 1);
     int nx = A.own_next[best];
     while (nx < lim) {
@@ -824,6 +855,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       M2 = __shfl_sync(0xffffffffu, M2, 0);
       if (M2 != M) break;  // a newer source block arrived: re-run EDF selection
     }
+    APROF(c_tile)
     __syncwarp();
     if (lane == 0) A.own_next[best] = nx;
     __syncwarp();
@@ -832,11 +864,21 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       __threadfence();
       __syncwarp();
       if (lane == 0) st_release_gpu(&P.ready[J], 1);
+#ifdef FABM_PROFILE
+      if (P.trace && lane == 0) P.trace[4 * J + 1] = global_ns();
+#endif
       cur = -1;
       ++done;
     }
   }
   if (lane == 0) atomicAdd(&P.ctrl->bulk_tiles, tiles);
+#ifdef FABM_PROFILE
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[4]), (unsigned long long)c_tile);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[5]), (unsigned long long)c_idle);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[6]), (unsigned long long)c_sw);
+  }
+#endif
 }
 
 // ======================================================================
@@ -848,7 +890,10 @@ __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P)
   } else {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     AgentSmem* A = reinterpret_cast<AgentSmem*>(smem_raw) + warp;
-    bulk_agent<D>(P, *A, (blockIdx.x - 1) * kWarps + warp, lane);
+    // agents are dealt warp-major across CTAs so every SM hosts a mix of
+    // light and heavy owners: when light agents finish, the heavy ones on the
+    // same SM inherit its FP64 throughput
+    bulk_agent<D>(P, *A, warp * (gridDim.x - 1) + (blockIdx.x - 1), lane);
   }
 }
 

@@ -146,6 +146,16 @@ static unsigned long long g_last_prof[8];
 extern "C" void fabm_debug_prof(unsigned long long* out) {
   for (int i = 0; i < 8; ++i) out[i] = g_last_prof[i];
 }
+#ifdef FABM_PROFILE
+static unsigned long long* g_trace = nullptr;
+static int g_trace_n = 0;
+extern "C" int fabm_debug_trace(unsigned long long* out, int n) {
+  if (!g_trace) return 0;
+  const int m = n < g_trace_n ? n : g_trace_n;
+  cudaMemcpy(out, g_trace, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost);
+  return m;
+}
+#endif
 
 struct fabm_plan {
   int device = 0;
@@ -352,6 +362,15 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   std::memcpy(P.params, p->prob.params, sizeof(P.params));
   P.nb = p->nb;
   P.n_agents = p->bulk_ctas * kWarps;
+#ifdef FABM_PROFILE
+  if (g_trace_n < 4 * (p->nb + 1)) {
+    if (g_trace) cudaFree(g_trace);
+    g_trace_n = 4 * (p->nb + 1);
+    cudaMalloc(&g_trace, sizeof(unsigned long long) * g_trace_n);
+  }
+  cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * g_trace_n, p->stream);
+  P.trace = g_trace;
+#endif
   const double tmo = timeout_s > 0 ? timeout_s : 60.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   if (const char* dbg = getenv("FABM_DEBUG_MODE")) P.debug = atoi(dbg);

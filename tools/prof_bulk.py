@@ -1,0 +1,18 @@
+import ctypes, os, sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1611_08678_b200 as fabm
+from paper_1611_08678_b200 import _native as nat
+lib = nat.load()
+for N in [int(x) for x in (sys.argv[1:] or ["300000", "1000000"])]:
+    p = fabm.FractionalProblem(alpha=0.99, dim=3, rhs=fabm.rhs_lorenz(), y0=(1., 1., 1.), t_end=100.0)
+    plan = fabm.GpuPlan(p, p.grid(N))
+    ms = plan.run()
+    buf = (ctypes.c_ulonglong * 8)()
+    lib.fabm_debug_prof(buf)
+    st = plan.stats()
+    agents = st["bulk_ctas"] * 16
+    cyc = ms * 1e-3 * 1.965e9
+    print(f"N={N} kernel={ms:.1f}ms steps/s={N/(ms*1e-3):.3e} wait={st['leader_wait_ns']/1e6:.1f}ms "
+          f"agents={agents} tile={buf[4]/agents/cyc:.3f} idle={buf[5]/agents/cyc:.3f} switch={buf[6]/agents/cyc:.3f} (fractions of kernel time per agent)", flush=True)
+    plan.close()
