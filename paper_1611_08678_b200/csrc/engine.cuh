@@ -70,6 +70,7 @@ struct EngineParams {
   const double* y0;        // device y0 (d doubles)
   double* Y;               // states (N+1) x d
   double* F;               // f history (nb*B + B) x DS
+  double* Fc;              // f_cache output, (N+1) x d compact
   double* BK;              // bulk accumulators (nb*B) x 2 x DS
   int* ready;              // per target block: bulk complete
   DevCtrl* ctrl;
@@ -546,8 +547,9 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
       ld_pairs<D>(&S.ring[ri][0], yf);
       double* yd = P.Y + k * D;
       double* fd = P.F + k * DS;
+      double* fo = P.Fc + k * D;
 #pragma unroll
-      for (int c = 0; c < D; ++c) { yd[c] = yf[c]; fd[c] = yf[D + c]; }
+      for (int c = 0; c < D; ++c) { yd[c] = yf[c]; fd[c] = yf[D + c]; fo[c] = yf[D + c]; }
     }
     __syncwarp();
     if (lane == 0) {

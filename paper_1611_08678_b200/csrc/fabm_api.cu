@@ -174,6 +174,7 @@ struct fabm_plan {
   double* y0 = nullptr;
   double* Y = nullptr;
   double* F = nullptr;
+  double* Fc = nullptr;
   double* BK = nullptr;
   int* ready = nullptr;
   DevCtrl* ctrl = nullptr;
@@ -190,7 +191,7 @@ static void plan_free(fabm_plan* p) {
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   for (void* ptr : {(void*)p->wb, (void*)p->wa, (void*)p->wc, (void*)p->y0, (void*)p->Y, (void*)p->F,
-                    (void*)p->BK, (void*)p->ready, (void*)p->ctrl})
+                    (void*)p->Fc, (void*)p->BK, (void*)p->ready, (void*)p->ctrl})
     if (ptr) cudaFree(ptr);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -267,6 +268,7 @@ fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid_i
   if ((e = cudaMalloc(&p->y0, sizeof(double) * FABM_MAX_DIM)) != cudaSuccess) return fail("malloc y0", e);
   if ((e = cudaMalloc(&p->Y, sizeof(double) * (p->N + 1) * problem->dim)) != cudaSuccess) return fail("malloc Y", e);
   if ((e = cudaMalloc(&p->F, sizeof(double) * fl)) != cudaSuccess) return fail("malloc F", e);
+  if ((e = cudaMalloc(&p->Fc, sizeof(double) * (p->N + 1) * problem->dim)) != cudaSuccess) return fail("malloc Fc", e);
   if ((e = cudaMalloc(&p->BK, sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds)) != cudaSuccess)
     return fail("malloc BK", e);
   if ((e = cudaMalloc(&p->ready, sizeof(int) * (p->nb + 1))) != cudaSuccess) return fail("malloc ready", e);
@@ -356,6 +358,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   P.y0 = p->y0;
   P.Y = p->Y;
   P.F = p->F;
+  P.Fc = p->Fc;
   P.BK = p->BK;
   P.ready = p->ready;
   P.ctrl = p->ctrl;
@@ -414,8 +417,7 @@ int fabm_plan_download(fabm_plan* p, double* states, double* f_cache, fabm_statu
   if (states)
     CUDA_TRY(cudaMemcpyAsync(states, p->Y, sizeof(double) * (p->N + 1) * d, cudaMemcpyDeviceToHost, p->stream));
   if (f_cache)
-    CUDA_TRY(cudaMemcpy2DAsync(f_cache, sizeof(double) * d, p->F, sizeof(double) * p->ds, sizeof(double) * d,
-                               p->N + 1, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(f_cache, p->Fc, sizeof(double) * (p->N + 1) * d, cudaMemcpyDeviceToHost, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   return FABM_OK;
 }

@@ -5,8 +5,8 @@ the reference factories (systems.py:26-123) — and attaches
 ``f.device_system = DeviceSystem(system_id, dim, params)``, which tells the
 GPU engine which compiled rhs to run (csrc/device_common.cuh ``Rhs<...>``).
 The host expression and the device expression use the same operator order,
-so f(t, y) agrees bit for bit between them (tests/test_systems.py checks
-that on the GPU).
+so f(t, y) agrees bit for bit between them (checked on the GPU by
+tests/test_gpu_parity.py::test_device_rhs_bitwise_equals_host).
 
 ``rhs_lorenz``/``rhs_chen``/``rhs_rossler``/``rhs_financial`` add the four
 BASELINE.json systems, which the reference does not ship.
@@ -34,6 +34,7 @@ __all__ = [
     "rhs_rossler",
     "rhs_financial",
     "device_system_of",
+    "adopt_reference_rhs",
 ]
 
 # must match FABM_SYS_* in include/fabm.h
@@ -69,16 +70,56 @@ def _tag(fn, name: str, dim, params):
     return fn
 
 
+def _closure_vars(fn) -> dict:
+    code = getattr(fn, "__code__", None)
+    cells = getattr(fn, "__closure__", None) or ()
+    if code is None:
+        return {}
+    return {name: cell.cell_contents for name, cell in zip(code.co_freevars, cells)}
+
+
+def adopt_reference_rhs(fn) -> DeviceSystem | None:
+    """Device tag for an rhs built by the reference's own factories.
+
+    ``fodeabm.systems.rhs_constant/rhs_power_law/rhs_linear/rhs_hindmarsh_rose``
+    (systems.py:26-123) return closures; their qualified name and captured
+    constants identify the system exactly, so problems built with the
+    reference API run on the device unchanged.  Anything else returns None.
+    """
+    if getattr(fn, "__module__", None) != "fodeabm.systems":
+        return None
+    qual = getattr(fn, "__qualname__", "")
+    env = _closure_vars(fn)
+    try:
+        if qual == "rhs_constant.<locals>.f":
+            vec = np.asarray(env["vec"], dtype=np.float64).reshape(-1)
+            return DeviceSystem("constant", len(vec), tuple(float(v) for v in vec))
+        if qual == "rhs_power_law.<locals>.f":
+            return DeviceSystem("power-law", 1, (float(env["coef"]), float(env["expo"])))
+        if qual == "rhs_linear.<locals>.f":
+            return DeviceSystem("linear", None, (float(env["lam"]),))
+        if qual == "rhs_hindmarsh_rose.<locals>.f":
+            names = ("a", "b", "c", "d", "r", "s", "x_rest", "i_ext")
+            return DeviceSystem("hindmarsh-rose", 3, tuple(float(env[n]) for n in names))
+    except (KeyError, TypeError, ValueError):
+        return None
+    return None
+
+
 def device_system_of(rhs) -> DeviceSystem:
     """The device tag of ``rhs``; plain callables have none (no CPU fallback)."""
     tag = getattr(rhs, "device_system", None)
-    if not isinstance(tag, DeviceSystem):
-        raise ValueError(
-            "the GPU engine needs a device rhs: build it with one of the "
-            "paper_1611_08678_b200.systems factories (plain Python callables "
-            "cannot run on the device)"
-        )
-    return tag
+    if isinstance(tag, DeviceSystem):
+        return tag
+    tag = adopt_reference_rhs(rhs)
+    if tag is not None:
+        return tag
+    raise ValueError(
+        "the GPU engine needs a device rhs: build it with one of the "
+        "paper_1611_08678_b200.systems factories or the reference's own "
+        "fodeabm.systems factories (arbitrary Python callables cannot run on "
+        "the device)"
+    )
 
 
 def rhs_constant(value):

@@ -190,3 +190,31 @@ def test_accepts_reference_style_objects(fabm):
     traj = fabm.solve_gpu(p, grid, weights="reference")
     g = golden("c1_linear")
     assert normwise_dev(traj.states, g["states"]) <= TOL
+
+
+@pytest.mark.parametrize("factory,y0,alpha", [
+    ("rhs_lorenz", (1.0, 1.0, 1.0), 0.99),
+    ("rhs_chen", (-9.0, -5.0, 14.0), 0.9),
+    ("rhs_rossler", (0.5, 1.5, 0.1), 0.9),
+    ("rhs_financial", (2.0, 3.0, 2.0), 0.95),
+    ("rhs_hindmarsh_rose", (0.1, 0.2, 0.2), 0.9),
+])
+def test_device_rhs_bitwise_equals_host(fabm, factory, y0, alpha):
+    """f_cache rows are device rhs outputs: they equal the host rhs bit for bit."""
+    rhs = getattr(fabm, factory)()
+    problem = fabm.FractionalProblem(alpha=alpha, dim=3, rhs=rhs, y0=y0, t_end=0.05)
+    grid = problem.grid(500)
+    traj = fabm.solve_gpu(problem, grid)
+    t = grid.times()
+    host = np.array([np.asarray(rhs(t[i], traj.states[i]), dtype=np.float64) for i in range(len(t))])
+    assert np.array_equal(host, traj.f_cache)
+
+
+def test_power_law_device_rhs_bitwise(fabm):
+    rhs = fabm.rhs_power_law(0.5, 2.0)
+    problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=rhs, y0=[0.0], t_end=1.0)
+    grid = problem.grid(300)
+    traj = fabm.solve_gpu(problem, grid)
+    host = np.array([rhs(ti, None)[0] for ti in grid.times()])
+    # CUDA pow vs libm pow may differ by an ulp; the reference tolerance is 1e-14 here
+    np.testing.assert_allclose(traj.f_cache[:, 0], host, rtol=2e-16 * 4, atol=0)

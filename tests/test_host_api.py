@@ -150,3 +150,39 @@ class TestSolverFrontEnd:
         for path in pkg.rglob("*.py"):
             text = path.read_text()
             assert "import oracle" not in text and "from oracle" not in text, path
+
+
+class TestReferenceInterop:
+    """Problems built with the reference's own factories are recognised."""
+
+    @pytest.fixture()
+    def fodeabm(self):
+        import sys
+        from pathlib import Path
+
+        src = Path("/root/reference/pkg/src")
+        if not src.exists():
+            pytest.skip("reference package not present (GPU box)")
+        sys.path.insert(0, str(src))
+        import fodeabm as ref
+
+        return ref
+
+    def test_adopts_reference_factories(self, fodeabm):
+        from paper_1611_08678_b200.systems import adopt_reference_rhs
+
+        t = adopt_reference_rhs(fodeabm.rhs_linear(-0.5))
+        assert t.name == "linear" and t.params == (-0.5,)
+        t = adopt_reference_rhs(fodeabm.rhs_constant([1.0, 2.0]))
+        assert t.name == "constant" and t.params == (1.0, 2.0) and t.dim == 2
+        t = adopt_reference_rhs(fodeabm.rhs_power_law(0.5, 2.0))
+        assert t.name == "power-law" and t.params[1] == 1.5
+        t = adopt_reference_rhs(fodeabm.rhs_hindmarsh_rose())
+        assert t.name == "hindmarsh-rose" and t.params[-1] == 3.25
+        assert adopt_reference_rhs(lambda t, y: y) is None
+
+    def test_reference_rhs_matches_ours(self, fodeabm):
+        ours = fabm.rhs_hindmarsh_rose()
+        theirs = fodeabm.rhs_hindmarsh_rose()
+        for y in ((0.1, 0.2, 0.3), (-1.3, 2.0, 0.7)):
+            assert ours(0.0, y) == theirs(0.0, y)
