@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--n", type=int, default=N_STEPS, help="ODE steps per trajectory")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU sample budget")
+    ap.add_argument("--workload", default="lorenz", choices=["lorenz", "batch"],
+                    help="lorenz: headline single trajectory (default); batch: BASELINE config 4 alpha sweep")
+    ap.add_argument("--batch-size", type=int, default=4096, help="trajectories in the config 4 sweep")
     return ap.parse_args()
 
 
@@ -371,10 +374,64 @@ def run_fabm(args, world, rank, local):
     print(json.dumps(out))
 
 
+def run_batch(args, world, rank, local):
+    """BASELINE config 4: financial system, alphas = 0.9 + 0.1*i/T, y0 = (2,3,2),
+    T=100, N=1e5 per trajectory; the sweep is sharded over ranks (contiguous
+    slices), NCCL all-gathers y_N.  Strong scaling (fixed total sweep)."""
+    import torch
+
+    import paper_1611_08678_b200 as fabm
+    from paper_1611_08678_b200 import parallel
+
+    torch.cuda.set_device(local)
+    n = args.n if args.n != N_STEPS else 100_000
+    T = args.batch_size
+    lo, hi = parallel.shard_bounds(T, world, rank)
+    rhs = fabm.rhs_financial()
+    h = 100.0 / n
+    probs = [fabm.FractionalProblem(alpha=0.9 + 0.1 * i / T, dim=3, rhs=rhs, y0=(2.0, 3.0, 2.0), t_end=100.0)
+             for i in range(lo, hi)]
+    grid = fabm.GridSpec(n_steps=n, h=h)
+    for _ in range(args.warmup):
+        fabm.solve_batch_gpu(probs, grid, states=False, device=local)
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier(world)
+    kms = []
+    for _ in range(args.steps):
+        res = fabm.solve_batch_gpu(probs, grid, states=False, device=local)
+        kms.append(res.kernel_ms)
+    barrier(world)
+    clocks = sampler.stop()
+    step_ms = max_over_ranks(world, float(np.mean(kms)))
+    value = T * n / (step_ms * 1e-3)
+    y_all = parallel.gather_rows(res.y_last, T, world, rank)
+    if rank != 0:
+        return
+    peak_fma = fabm.measure_dfma_peak(local)
+    fma = 3.0 * n * n * T
+    achieved = 2.0 * fma / (step_ms * 1e-3) / 1e12 / world
+    print(json.dumps({
+        "metric": "ABM trajectory-steps/sec, financial alpha sweep (BASELINE config 4)",
+        "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (deterministic financial IVPs)",
+        "config": {"workload": f"financial alpha sweep T={T} N={n}", "trajectories": T, "n_steps": n,
+                   "parallelism": f"trajectory shards x{world}"},
+        "history_fma_per_s": fma / (step_ms * 1e-3),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": 2.0 * peak_fma / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / (2.0 * peak_fma / 1e12), "traffic": None},
+        "gpu_launches": 2 * args.steps, "clocks": clocks,
+        "y_N_checksum": float(np.sum(y_all)),
+    }))
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup(args)
-    if args.impl == "reference":
+    if args.workload == "batch":
+        run_batch(args, world, rank, local)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_fabm(args, world, rank, local)

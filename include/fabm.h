@@ -103,6 +103,7 @@ typedef struct fabm_status {
   int32_t kind;      /* FABM_KIND_* for FABM_ERR_NONFINITE           */
   int64_t step;      /* loop index n of the failing step             */
   double t;          /* (n + 1) * h                                  */
+  int64_t index;     /* batch: lowest failing trajectory (else -1)   */
   char message[240];
 } fabm_status;
 
@@ -160,12 +161,19 @@ int fabm_plan_stats(const fabm_plan* plan, fabm_stats* stats);
 void fabm_plan_destroy(fabm_plan* plan);
 
 /* ---- batch: many independent trajectories (BASELINE config 4) ----------
- * problems[count], grids[count] share n_steps and h; states/f_cache (may be
- * NULL for f_cache) hold count*(n_steps+1)*dim doubles, trajectory-major.
- * Weights are generated on device per trajectory (alpha differs). */
+ * A sweep of `count` problems is `count` solve_serial calls in the reference
+ * (serial.py:114-176).  problems[count] and grids[count] must share dim,
+ * system, n_steps and h; alpha, y0, params and the per-solve scalars may
+ * differ.  Weights are generated on the device per trajectory (ACCURATE).
+ * Outputs (host, trajectory-major, any may be NULL):
+ *   states, f_cache : count*(n_steps+1)*dim doubles
+ *   y_last          : count*dim doubles (y_N of every trajectory)
+ * A non-finite rhs stops that trajectory only; the status reports the
+ * lowest failing index (status.index), its step and t. */
 int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids,
                      int64_t count, int device, double* states,
-                     double* f_cache, double* kernel_ms, fabm_status* status);
+                     double* f_cache, double* y_last, double* kernel_ms,
+                     fabm_status* status);
 
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
 /* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */

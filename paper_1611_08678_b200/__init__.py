@@ -32,7 +32,7 @@ from .systems import (
     rhs_power_law,
     rhs_rossler,
 )
-from .solver import GpuPlan, device_count, measure_dfma_peak, solve_gpu
+from .solver import BatchResult, GpuPlan, device_count, measure_dfma_peak, solve_batch_gpu, solve_gpu
 
 __version__ = "0.1.0"
 
@@ -49,6 +49,8 @@ __all__ = [
     "corrector_weight_c",
     "precompute_weights",
     "solve_gpu",
+    "solve_batch_gpu",
+    "BatchResult",
     "GpuPlan",
     "device_count",
     "measure_dfma_peak",

@@ -78,6 +78,7 @@ class Status(ctypes.Structure):
         ("kind", ctypes.c_int32),
         ("step", ctypes.c_int64),
         ("t", ctypes.c_double),
+        ("index", ctypes.c_int64),
         ("message", ctypes.c_char * 240),
     ]
 
@@ -122,7 +123,7 @@ def _declare(lib):
         "fabm_plan_download_last": (ctypes.c_int, [plan, _DP, S]),
         "fabm_plan_stats": (ctypes.c_int, [plan, St]),
         "fabm_plan_destroy": (None, [plan]),
-        "fabm_solve_batch": (ctypes.c_int, [P, G, ctypes.c_int64, ctypes.c_int, _DP, _DP, _DP, S]),
+        "fabm_solve_batch": (ctypes.c_int, [P, G, ctypes.c_int64, ctypes.c_int, _DP, _DP, _DP, _DP, S]),
         "fabm_measure_dfma_peak": (ctypes.c_double, [ctypes.c_int]),
     }
     for name, (res, args) in sig.items():

@@ -1,0 +1,231 @@
+// batch.cuh — many independent trajectories (BASELINE config 4: the
+// fractional financial system swept over 4096 orders alpha, N = 1e5).
+//
+// The reference integrates each problem with solve_serial (serial.py:114-176);
+// a sweep is a loop of such calls.  Here one persistent kernel (one CTA per
+// SM, 16 warps) integrates the whole sweep.  Work is cut into UNITS
+// (trajectory t, block J of 128 steps); a warp takes units from a global
+// ticket counter in the order u -> (t = u mod T, J = u div T), so all
+// trajectories advance together and the last wave is evenly filled.  A unit:
+//   1. pulls the bulk of its 128 targets from every completed block I < J:
+//      J Toeplitz tiles (the same register-blocked tile as the single-
+//      trajectory agents) in ascending I — a fixed FMA order, independent of
+//      which warp runs the unit, so results are bitwise deterministic;
+//   2. steps through the block: all 32 lanes run the sequential chain
+//      (serial.py:150-170) redundantly; lane l holds the sums of steps
+//      JB+4l..JB+4l+3 and pushes every new f_k into them (in-block window).
+// A unit waits (acquire) until unit (t, J-1) released the block J-1 rows;
+// that unit holds an earlier ticket, so its warp is already running.
+#pragma once
+#include "engine.cuh"
+
+namespace fabm {
+
+struct BatchParams {
+  int T;                    // trajectories
+  int nb;                   // blocks per trajectory
+  long long N;              // steps
+  long long WL;             // weight row length per trajectory (nb*B + 2B)
+  double h;
+  const double* ha;         // [T] h^alpha
+  const double* ig;         // [T] 1/Gamma(alpha+2)
+  const double* y0;         // [T][kMaxDim]
+  const double* params;     // [T][kMaxParams]
+  const double* W;          // [T][3][WL]: b, a, c
+  double* F;                // [T][(nb+1)*B][DS]
+  double* Y;                // [T][N+1][D] or null
+  double* Fc;               // [T][N+1][D] or null
+  double* ylast;            // [T][D]: y_N
+  int* next_block;          // [T]: blocks completed (release)
+  int* err_kind;            // [T]
+  long long* err_step;      // [T]
+  unsigned long long* ticket;
+  unsigned long long timeout_ns;
+  DevCtrl* ctrl;
+};
+
+template <int SYS, int D>
+__device__ void batch_unit(const BatchParams& P, AgentSmem& A, int t, int J, int lane) {
+  constexpr int DS = Stride<D>::value;
+  const long long N = P.N;
+  const double* wb = P.W + static_cast<long long>(t) * 3 * P.WL;
+  const double* wa = wb + P.WL;
+  const double* wc = wa + P.WL;
+  double* F = P.F + static_cast<long long>(t) * (P.nb + 1) * kB * DS;
+  double* Y = P.Y ? P.Y + static_cast<long long>(t) * (N + 1) * D : nullptr;
+  double* Fc = P.Fc ? P.Fc + static_cast<long long>(t) * (N + 1) * D : nullptr;
+  const double* prm = P.params + static_cast<long long>(t) * kMaxParams;
+  double params[kMaxParams];
+#pragma unroll
+  for (int i = 0; i < kMaxParams; ++i) params[i] = prm[i];
+  double y0[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) y0[c] = P.y0[t * kMaxDim + c];
+  const double ha = P.ha[t], ig = P.ig[t];
+  const long long JB = static_cast<long long>(J) * kB;
+
+  // ---- 1. bulk of sources I < J (ascending), in registers
+  double accP[kR][D], accC[kR][D];
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+#pragma unroll
+    for (int c = 0; c < D; ++c) { accP[r][c] = 0.0; accC[r][c] = 0.0; }
+  for (int I = 0; I < J; ++I) agent_tile<D>(wb, wa, F, A, I, J, lane, accP, accC);
+  __syncwarp();
+
+  // ---- 2. state at the block start: f_JB (and f_0), first-node terms
+  double f0[D], fc[D];
+  if (J == 0) {
+    Rhs<SYS, D>::eval(0.0, y0, f0, params);
+#pragma unroll
+    for (int c = 0; c < D; ++c) fc[c] = f0[c];
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        F[c] = f0[c];
+        if (Y) Y[c] = y0[c];
+        if (Fc) Fc[c] = f0[c];
+      }
+    }
+    if (any_nonfinite<D>(f0)) {
+      if (lane == 0) { P.err_kind[t] = KIND_INITIAL; P.err_step[t] = 0; }
+      return;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; ++c) { f0[c] = __ldcg(F + c); fc[c] = __ldcg(F + JB * DS + c); }
+  }
+  // in-block weights: tb[j + 128] = b_j for 1 <= j < B, 0 otherwise (A.f is free now)
+  double* tb = &A.f[0][0];
+  double* ta = tb + 2 * kB;
+  for (int i = lane; i < 2 * kB; i += 32) {
+    const int j = i - kB;
+    tb[i] = (j >= 1) ? __ldg(wb + j) : 0.0;
+    ta[i] = (j >= 1) ? __ldg(wa + j) : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const long long m = JB + kR * lane + r;
+    // J >= 1: the bulk includes k = 0 in the a-sum -> (c_m - a_m) f0; J = 0:
+    // the window excludes k = 0 from the a-sum -> c_m f0
+    const double cf = m < N ? (J >= 1 ? __ldg(wc + m) - __ldg(wa + m) : __ldg(wc + m)) : 0.0;
+#pragma unroll
+    for (int c = 0; c < D; ++c) accC[r][c] = add_rn(accC[r][c], mul_rn(cf, f0[c]));
+  }
+  __syncwarp();
+  if (J == 0) {
+    // f_0 enters the sums of steps 1..B-1 (b only; k = 0 is not interior)
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const double w = tb[kR * lane + r + kB];
+#pragma unroll
+      for (int c = 0; c < D; ++c) accP[r][c] = fma(w, f0[c], accP[r][c]);
+    }
+  }
+  const double b0 = __ldg(wb), a0 = __ldg(wa);
+
+  // ---- 3. the sequential chain over the block
+  const long long nend = (JB + kB < N) ? JB + kB : N;
+  int ekind = KIND_NONE;
+  long long estep = -1;
+  for (long long n = JB; n < nend; ++n) {
+    const int i = static_cast<int>(n - JB);
+    const int owner = i >> 2, rr = i & 3;
+    // pre-sums of step n from the owner lane (r is warp-uniform)
+    double pP[D], pC[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      double vp = accP[0][c], vc = accC[0][c];
+#pragma unroll
+      for (int r = 1; r < kR; ++r) {
+        vp = rr == r ? accP[r][c] : vp;
+        vc = rr == r ? accC[r][c] : vc;
+      }
+      pP[c] = __shfl_sync(0xffffffffu, vp, owner);
+      pC[c] = __shfl_sync(0xffffffffu, vc, owner);
+    }
+    const double t1 = static_cast<double>(n + 1) * P.h;
+    const double a0e = n >= 1 ? a0 : 0.0;
+    double yP[D], fP[D], y1[D], f1[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(b0, fc[c], pP[c]), ha), y0[c]);
+    Rhs<SYS, D>::eval(t1, yP, fP, params);
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+      y1[c] = add_rn(mul_rn(add_rn(fma(a0e, fc[c], pC[c]), mul_rn(ig, fP[c])), ha), y0[c]);
+    Rhs<SYS, D>::eval(t1, y1, f1, params);
+    const bool bp = any_nonfinite<D>(fP), bc = any_nonfinite<D>(f1);
+    const int kind = bp ? KIND_PREDICTOR : (bc ? KIND_CORRECTOR : KIND_NONE);
+    const bool first = (kind != KIND_NONE) & (ekind == KIND_NONE);
+    ekind = first ? kind : ekind;
+    estep = first ? n : estep;
+    // rows y_{n+1}, f_{n+1}
+    if (lane == ((i + 1) & 31)) {
+      double* fd = F + (n + 1) * DS;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        fd[c] = f1[c];
+        if (Y) Y[(n + 1) * D + c] = y1[c];
+        if (Fc) Fc[(n + 1) * D + c] = f1[c];
+        if (n + 1 == N) P.ylast[t * D + c] = y1[c];
+      }
+    }
+    // push f_{n+1} into the steps m > n+1 of this block
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const int j = kR * lane + r - (i + 1);  // m - (n+1)
+      const double w1 = tb[j + kB], w2 = ta[j + kB];
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        accP[r][c] = fma(w1, f1[c], accP[r][c]);
+        accC[r][c] = fma(w2, f1[c], accC[r][c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < D; ++c) fc[c] = f1[c];
+    if ((i & 7) == 7 && ekind != KIND_NONE) break;
+  }
+  if (ekind != KIND_NONE && lane == 0) {
+    P.err_kind[t] = ekind;
+    P.err_step[t] = estep;
+  }
+}
+
+template <int SYS, int D>
+__global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  AgentSmem& A = reinterpret_cast<AgentSmem*>(smem_raw)[warp];
+  const unsigned long long total = static_cast<unsigned long long>(P.T) * P.nb;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(P.ticket, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= total) break;
+    const int t = static_cast<int>(u % P.T), J = static_cast<int>(u / P.T);
+    if (J > 0) {
+      // unit (t, J-1) holds an earlier ticket: its warp is running
+      int done = 0;
+      const unsigned long long w0 = global_ns();
+      for (;;) {
+        if (lane == 0) done = ld_acquire_gpu(&P.next_block[t]);
+        done = __shfl_sync(0xffffffffu, done, 0);
+        if (done >= J) break;
+        if (*((volatile int*)&P.ctrl->abort)) return;
+        if (global_ns() - w0 > P.timeout_ns) {
+          if (lane == 0) ctrl_abort(P.ctrl, ERR_TIMEOUT, KIND_NONE, -1, 0.0);
+          return;
+        }
+        __nanosleep(200);
+      }
+      __syncwarp();
+    }
+    const bool dead = *((volatile int*)&P.err_kind[t]) != KIND_NONE;
+    if (!dead) batch_unit<SYS, D>(P, A, t, J, lane);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_gpu(&P.next_block[t], J + 1);
+  }
+}
+
+}  // namespace fabm

@@ -88,14 +88,17 @@ __device__ __forceinline__ long long lo_of(long long m) {
   return lb > 0 ? lb * kB : 0;
 }
 
-__device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int kind, long long step, double t) {
-  if (atomicCAS(&P.ctrl->err_code, 0, code) == 0) {
-    P.ctrl->err_kind = kind;
-    P.ctrl->err_step = step;
-    P.ctrl->err_t = t;
+__device__ __forceinline__ void ctrl_abort(DevCtrl* ctrl, int code, int kind, long long step, double t) {
+  if (atomicCAS(&ctrl->err_code, 0, code) == 0) {
+    ctrl->err_kind = kind;
+    ctrl->err_step = step;
+    ctrl->err_t = t;
   }
   __threadfence();
-  atomicExch(&P.ctrl->abort, 1);
+  atomicExch(&ctrl->abort, 1);
+}
+__device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int kind, long long step, double t) {
+  ctrl_abort(P.ctrl, code, kind, step, t);
 }
 
 // ======================================================================
@@ -707,20 +710,21 @@ __device__ __forceinline__ void agent_load_acc(const EngineParams& P, int J, int
 // acc[n] += sum_{k in block I} w[n - k] f_k for the lane's 4 targets of block J,
 // ascending k.  Weight window u = 127 - s + r (jl = 4*lane + u), mod-4 transposed.
 template <int D>
-__device__ __forceinline__ void agent_tile(const EngineParams& P, AgentSmem& A, int I, int J, int lane,
+__device__ __forceinline__ void agent_tile(const double* __restrict__ wbp, const double* __restrict__ wap,
+                                           const double* Fp, AgentSmem& A, int I, int J, int lane,
                                            double (&accP)[kR][D], double (&accC)[kR][D]) {
   constexpr int DS = Stride<D>::value;
   __syncwarp();
   // ---- stage weights j in [Delta-127, Delta+127] (transposed) and the f tile
   const long long base = static_cast<long long>(J - I) * kB - (kB - 1);
   for (int jl = lane; jl < 2 * kB - 1; jl += 32) {
-    const double vb = __ldg(P.wb + base + jl);
-    const double va = __ldg(P.wa + base + jl);
+    const double vb = __ldg(wbp + base + jl);
+    const double va = __ldg(wap + base + jl);
     A.w[0][jl & 3][jl >> 2] = vb;
     A.w[1][jl & 3][jl >> 2] = va;
   }
   {
-    const double* src = P.F + static_cast<long long>(I) * kB * DS;
+    const double* src = Fp + static_cast<long long>(I) * kB * DS;
     if constexpr (DS >= 2) {
       for (int i = lane; i < kB * DS / 2; i += 32) {
         const double2 v = __ldcg(reinterpret_cast<const double2*>(src) + i);
@@ -851,7 +855,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     while (nx < lim) {
       int M2 = 0;
       if (lane == 0) M2 = ld_relaxed_gpu(&P.ctrl->src_done);
-      agent_tile<D>(P, A, nx, J, lane, accP, accC);
+      agent_tile<D>(P.wb, P.wa, P.F, A, nx, J, lane, accP, accC);
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);

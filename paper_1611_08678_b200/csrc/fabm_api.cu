@@ -11,8 +11,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "../../include/fabm.h"
+#include "batch.cuh"
 #include "engine.cuh"
 #include "weights.cuh"
 
@@ -485,12 +487,226 @@ int fabm_weights(double alpha, int64_t n_steps, int mode, double gamma1, double 
   return FABM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+using BatchLaunch = cudaError_t (*)(const BatchParams&, int grid, cudaStream_t);
+
+template <int SYS, int D>
+cudaError_t launch_batch(const BatchParams& P, int grid, cudaStream_t stream) {
+  auto kern = abm_batch_kernel<SYS, D>;
+  const size_t smem = kWarps * sizeof(AgentSmem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, smem, stream>>>(P);
+  return cudaGetLastError();
+}
+
+BatchLaunch pick_batch(int sys, int dim) {
+  switch (sys) {
+    case FABM_SYS_CONSTANT:
+      switch (dim) {
+        case 1: return launch_batch<SYS_CONSTANT, 1>;
+        case 2: return launch_batch<SYS_CONSTANT, 2>;
+        case 3: return launch_batch<SYS_CONSTANT, 3>;
+        case 4: return launch_batch<SYS_CONSTANT, 4>;
+      }
+      break;
+    case FABM_SYS_LINEAR:
+      switch (dim) {
+        case 1: return launch_batch<SYS_LINEAR, 1>;
+        case 2: return launch_batch<SYS_LINEAR, 2>;
+        case 3: return launch_batch<SYS_LINEAR, 3>;
+        case 4: return launch_batch<SYS_LINEAR, 4>;
+      }
+      break;
+    case FABM_SYS_POWER_LAW: return launch_batch<SYS_POWER_LAW, 1>;
+    case FABM_SYS_HINDMARSH_ROSE: return launch_batch<SYS_HINDMARSH_ROSE, 3>;
+    case FABM_SYS_LORENZ: return launch_batch<SYS_LORENZ, 3>;
+    case FABM_SYS_CHEN: return launch_batch<SYS_CHEN, 3>;
+    case FABM_SYS_ROSSLER: return launch_batch<SYS_ROSSLER, 3>;
+    case FABM_SYS_FINANCIAL: return launch_batch<SYS_FINANCIAL, 3>;
+  }
+  return nullptr;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+}  // namespace
+
+extern "C" {
+
 int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64_t count, int device, double* states,
-                     double* f_cache, double* kernel_ms, fabm_status* status) {
-  (void)problems; (void)grids; (void)count; (void)device; (void)states; (void)f_cache; (void)kernel_ms;
+                     double* f_cache, double* y_last, double* kernel_ms, fabm_status* status) {
   clear_status(status);
-  set_status(status, FABM_ERR_CONFIG, "batch engine not built");
-  return FABM_ERR_CONFIG;
+  if (status) status->index = -1;
+  if (!problems || !grids || count < 1) {
+    set_status(status, FABM_ERR_CONFIG, "batch needs count >= 1 problems and grids");
+    return FABM_ERR_CONFIG;
+  }
+  if (count > (1LL << 30)) {
+    set_status(status, FABM_ERR_CONFIG, "batch too large");
+    return FABM_ERR_CONFIG;
+  }
+  const int T = static_cast<int>(count);
+  const fabm_problem& p0 = problems[0];
+  const long long N = grids[0].n_steps;
+  for (int t = 0; t < T; ++t) {
+    int rc = validate(&problems[t], &grids[t], status);
+    if (rc != FABM_OK) {
+      if (status) status->index = t;
+      return rc;
+    }
+    if (problems[t].dim != p0.dim || problems[t].system != p0.system || grids[t].n_steps != N ||
+        grids[t].h != grids[0].h) {
+      set_status(status, FABM_ERR_CONFIG, "batch members must share dim, system, n_steps and h (member %d)", t);
+      if (status) status->index = t;
+      return FABM_ERR_CONFIG;
+    }
+  }
+  const int D = p0.dim, DS = stride_of(D);
+  BatchLaunch launch = pick_batch(p0.system, D);
+  if (!launch) { set_status(status, FABM_ERR_CONFIG, "no batch engine for system/dim"); return FABM_ERR_CONFIG; }
+  int ndev = fabm_device_count();
+  if (ndev <= 0 || device < 0 || device >= ndev) {
+    set_status(status, FABM_ERR_NODEVICE, "no CUDA device %d (found %d)", device, ndev);
+    return FABM_ERR_NODEVICE;
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  const int nb = static_cast<int>((N + kB - 1) / kB);
+  const long long WL = static_cast<long long>(nb) * kB + 2 * kB;
+  // host-side per-trajectory scalars (the caller's CPython values when given)
+  std::vector<double> hal(T), hg1(T), hg2(T), hha(T), hig(T), hy0(static_cast<size_t>(T) * kMaxDim, 0.0),
+      hprm(static_cast<size_t>(T) * kMaxParams, 0.0);
+  for (int t = 0; t < T; ++t) {
+    fabm_grid g = grids[t];
+    fill_scalars(&problems[t], &g);
+    hal[t] = problems[t].alpha;
+    hg1[t] = g.gamma1;
+    hg2[t] = g.gamma2;
+    hha[t] = g.h_alpha;
+    hig[t] = g.inv_gamma2;
+    for (int c = 0; c < D; ++c) hy0[static_cast<size_t>(t) * kMaxDim + c] = problems[t].y0[c];
+    for (int i = 0; i < kMaxParams; ++i) hprm[static_cast<size_t>(t) * kMaxParams + i] = problems[t].params[i];
+  }
+  DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl;
+  const size_t szF = sizeof(double) * static_cast<size_t>(T) * (nb + 1) * kB * DS;
+  const size_t szY = sizeof(double) * static_cast<size_t>(T) * (N + 1) * D;
+  CUDA_TRY(cudaMalloc(&dal.p, sizeof(double) * T));
+  CUDA_TRY(cudaMalloc(&dg1.p, sizeof(double) * T));
+  CUDA_TRY(cudaMalloc(&dg2.p, sizeof(double) * T));
+  CUDA_TRY(cudaMalloc(&dha.p, sizeof(double) * T));
+  CUDA_TRY(cudaMalloc(&dig.p, sizeof(double) * T));
+  CUDA_TRY(cudaMalloc(&dy0.p, sizeof(double) * hy0.size()));
+  CUDA_TRY(cudaMalloc(&dprm.p, sizeof(double) * hprm.size()));
+  CUDA_TRY(cudaMalloc(&dW.p, sizeof(double) * static_cast<size_t>(T) * 3 * WL));
+  CUDA_TRY(cudaMalloc(&dF.p, szF));
+  if (states) CUDA_TRY(cudaMalloc(&dY.p, szY));
+  if (f_cache) CUDA_TRY(cudaMalloc(&dFc.p, szY));
+  CUDA_TRY(cudaMalloc(&dyl.p, sizeof(double) * static_cast<size_t>(T) * D));
+  CUDA_TRY(cudaMalloc(&dnext.p, sizeof(int) * T));
+  CUDA_TRY(cudaMalloc(&dek.p, sizeof(int) * T));
+  CUDA_TRY(cudaMalloc(&des.p, sizeof(long long) * T));
+  CUDA_TRY(cudaMalloc(&dtk.p, sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&dctrl.p, sizeof(DevCtrl)));
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto cleanup = [&]() {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(stream);
+  };
+  cudaMemcpyAsync(dal.p, hal.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dg1.p, hg1.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dg2.p, hg2.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dha.p, hha.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dig.p, hig.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dy0.p, hy0.data(), sizeof(double) * hy0.size(), cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dprm.p, hprm.data(), sizeof(double) * hprm.size(), cudaMemcpyHostToDevice, stream);
+  cudaMemsetAsync(dF.p, 0, szF, stream);
+  cudaMemsetAsync(dnext.p, 0, sizeof(int) * T, stream);
+  cudaMemsetAsync(dek.p, 0, sizeof(int) * T, stream);
+  cudaMemsetAsync(des.p, 0, sizeof(long long) * T, stream);
+  cudaMemsetAsync(dtk.p, 0, sizeof(unsigned long long), stream);
+  cudaMemsetAsync(dctrl.p, 0, sizeof(DevCtrl), stream);
+  {
+    const long long total = static_cast<long long>(T) * WL;
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 64));
+    weights_batch_kernel<<<blocks, 256, 0, stream>>>(dal.as<double>(), dg1.as<double>(), dg2.as<double>(), T, WL,
+                                                     dW.as<double>());
+  }
+  BatchParams P{};
+  P.T = T;
+  P.nb = nb;
+  P.N = N;
+  P.WL = WL;
+  P.h = grids[0].h;
+  P.ha = dha.as<double>();
+  P.ig = dig.as<double>();
+  P.y0 = dy0.as<double>();
+  P.params = dprm.as<double>();
+  P.W = dW.as<double>();
+  P.F = dF.as<double>();
+  P.Y = dY.as<double>();
+  P.Fc = dFc.as<double>();
+  P.ylast = dyl.as<double>();
+  P.next_block = dnext.as<int>();
+  P.err_kind = dek.as<int>();
+  P.err_step = des.as<long long>();
+  P.ticket = dtk.as<unsigned long long>();
+  P.timeout_ns = 600ull * 1000000000ull;
+  P.ctrl = dctrl.as<DevCtrl>();
+  cudaEventRecord(e0, stream);
+  cudaError_t le = launch(P, prop.multiProcessorCount, stream);
+  cudaEventRecord(e1, stream);
+  cudaError_t se = cudaStreamSynchronize(stream);
+  if (le != cudaSuccess || se != cudaSuccess) {
+    set_status(status, FABM_ERR_CUDA, "batch kernel: %s", cudaGetErrorString(le != cudaSuccess ? le : se));
+    cleanup();
+    return FABM_ERR_CUDA;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  if (kernel_ms) *kernel_ms = ms;
+  if (states) cudaMemcpy(states, dY.p, szY, cudaMemcpyDeviceToHost);
+  if (f_cache) cudaMemcpy(f_cache, dFc.p, szY, cudaMemcpyDeviceToHost);
+  if (y_last) cudaMemcpy(y_last, dyl.p, sizeof(double) * static_cast<size_t>(T) * D, cudaMemcpyDeviceToHost);
+  std::vector<int> hek(T);
+  std::vector<long long> hes(T);
+  cudaMemcpy(hek.data(), dek.p, sizeof(int) * T, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hes.data(), des.p, sizeof(long long) * T, cudaMemcpyDeviceToHost);
+  DevCtrl hc{};
+  cudaMemcpy(&hc, dctrl.p, sizeof(DevCtrl), cudaMemcpyDeviceToHost);
+  cleanup();
+  if (hc.err_code == ERR_TIMEOUT) {
+    set_status(status, FABM_ERR_TIMEOUT, "batch watchdog expired");
+    return FABM_ERR_TIMEOUT;
+  }
+  for (int t = 0; t < T; ++t) {
+    if (hek[t] != KIND_NONE) {
+      if (status) {
+        status->code = FABM_ERR_NONFINITE;
+        status->kind = hek[t];
+        status->step = hes[t];
+        status->t = hek[t] == KIND_INITIAL ? 0.0 : static_cast<double>(hes[t] + 1) * grids[0].h;
+        status->index = t;
+        snprintf(status->message, sizeof(status->message), "trajectory %d: rhs returned a non-finite value", t);
+      }
+      return FABM_ERR_NONFINITE;
+    }
+  }
+  return FABM_OK;
 }
 
 // ---------------------------------------------------------------- DFMA peak

@@ -95,4 +95,21 @@ __global__ void weights_kernel(double al, double g1, double g2, long long len, i
   }
 }
 
+// one weight table per trajectory: W[t] = {b[0..len), a[0..len), c[0..len)}
+__global__ void weights_batch_kernel(const double* __restrict__ alphas, const double* __restrict__ g1,
+                                     const double* __restrict__ g2, int T, long long len,
+                                     double* __restrict__ W) {
+  const long long total = static_cast<long long>(T) * len;
+  for (long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(q / len);
+    const long long n = q % len;
+    double* w = W + static_cast<long long>(t) * 3 * len;
+    const double al = alphas[t];
+    w[n] = weight_b_accurate(al, g1[t], n);
+    w[len + n] = weight_a_accurate(al, g2[t], n);
+    w[2 * len + n] = weight_c_accurate(al, g2[t], n);
+  }
+}
+
 }  // namespace fabm

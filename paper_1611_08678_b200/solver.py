@@ -28,7 +28,8 @@ from . import _native as nat
 from .core import GridSpec, SolverStepError, StrategyTimeoutError, Trajectory, precompute_weights
 from .systems import device_system_of
 
-__all__ = ["solve_gpu", "GpuPlan", "device_count", "measure_dfma_peak", "STRATEGY_NAME"]
+__all__ = ["solve_gpu", "solve_batch_gpu", "BatchResult", "GpuPlan", "device_count", "measure_dfma_peak",
+           "STRATEGY_NAME"]
 
 STRATEGY_NAME = "gpu"
 # the reference watchdog default (_shm.py:35); FABM_TIMEOUT_S overrides it
@@ -245,3 +246,86 @@ def solve_gpu(
         stats.update(plan.stats())
         stats["strategy"] = STRATEGY_NAME
     return traj
+
+
+class BatchResult:
+    """Outputs of :func:`solve_batch_gpu` (trajectory-major arrays, read-only)."""
+
+    def __init__(self, grid, states, f_cache, y_last, kernel_ms, error):
+        self.grid = grid
+        self.states = states
+        self.f_cache = f_cache
+        self.y_last = y_last
+        self.kernel_ms = kernel_ms
+        self.error = error  # None or (index, SolverStepError)
+        for arr in (states, f_cache, y_last):
+            if arr is not None:
+                arr.setflags(write=False)
+
+    def trajectory(self, i: int) -> Trajectory:
+        if self.states is None or self.f_cache is None:
+            raise ValueError("solve_batch_gpu was called without states/f_cache")
+        return Trajectory(grid=self.grid, states=self.states[i].copy(), f_cache=self.f_cache[i].copy())
+
+
+def solve_batch_gpu(
+    problems,
+    grid,
+    *,
+    states: bool = True,
+    f_cache: bool = False,
+    device: int = 0,
+    raise_on_error: bool = True,
+) -> BatchResult:
+    """Integrate many independent problems on one GPU (BASELINE config 4).
+
+    Equivalent to ``[solve_serial(p, grid) for p in problems]`` (serial.py:
+    114-176) with device-generated ACCURATE weights per problem.  All
+    problems must share the rhs system, dim, horizon and grid; alpha, y0 and
+    the rhs parameters may differ.  A non-finite rhs stops only its own
+    trajectory; with ``raise_on_error`` the lowest failing index is raised as
+    :class:`SolverStepError` (its ``index`` attribute names the trajectory).
+    """
+    problems = list(problems)
+    if not problems:
+        raise ValueError("solve_batch_gpu needs at least one problem")
+    N = int(grid.n_steps)
+    for p in problems:
+        if not grid.spans(p.t_end):
+            raise ValueError(f"grid (h={grid.h!r}, N={N}) does not span t_end={p.t_end!r}")
+    structs = [_structs(p, grid) for p in problems]
+    d = int(problems[0].dim)
+    T = len(problems)
+    probs = (nat.Problem * T)(*[s[0] for s in structs])
+    grids = (nat.Grid * T)(*[s[1] for s in structs])
+    st_arr = np.empty((T, N + 1, d)) if states else None
+    fc_arr = np.empty((T, N + 1, d)) if f_cache else None
+    y_last = np.empty((T, d))
+    ms = ctypes_double()
+    st = nat.Status()
+    rc = nat.load().fabm_solve_batch(probs, grids, T, int(device), nat.dptr(st_arr), nat.dptr(fc_arr),
+                                     nat.dptr(y_last), ctypes_ptr(ms), ctypes_ref(st))
+    error = None
+    if rc == nat.FABM_ERR_NONFINITE:
+        t = float(st.t)
+        exc = SolverStepError(f"trajectory {st.index}: rhs returned a non-finite value", step=int(st.step), t=t)
+        exc.index = int(st.index)
+        if raise_on_error:
+            raise exc
+        error = (int(st.index), exc)
+    elif rc != nat.FABM_OK:
+        _raise_status(st)
+    g = grid if isinstance(grid, GridSpec) else GridSpec(grid.n_steps, grid.h)
+    return BatchResult(g, st_arr, fc_arr, y_last, float(ms.value), error)
+
+
+def ctypes_double():
+    import ctypes
+
+    return ctypes.c_double(0.0)
+
+
+def ctypes_ptr(obj):
+    import ctypes
+
+    return ctypes.pointer(obj)

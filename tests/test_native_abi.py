@@ -58,7 +58,7 @@ def test_struct_layout_matches_header():
     # fabm_problem: double + 2*int32 + 16 doubles + 4 doubles
     assert ctypes.sizeof(_native.Problem) == 8 + 8 + 8 * 16 + 8 * 4
     assert ctypes.sizeof(_native.Grid) == 8 * 6
-    assert ctypes.sizeof(_native.Status) == 4 + 4 + 8 + 8 + 240
+    assert ctypes.sizeof(_native.Status) == 4 + 4 + 8 + 8 + 8 + 240
 
 
 def test_config_errors_need_no_device(lib):

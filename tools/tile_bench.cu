@@ -20,7 +20,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_kernel(EngineParams P, int t
   for (int t = 0; t < tiles; ++t) {
     const int J = 3 + (agent * 7 + t * 13) % (P.nb - 3);
     const int I = (agent + t) % (J - 2);
-    agent_tile<D>(P, *A, I, J, lane, accP, accC);
+    agent_tile<D>(P.wb, P.wa, P.F, *A, I, J, lane, accP, accC);
   }
   double s = 0;
   for (int r = 0; r < kR; ++r)
