@@ -113,13 +113,16 @@ __device__ void batch_unit(const BatchParams& P, AgentSmem& A, int t, int J, int
     for (int c = 0; c < D; ++c) accC[r][c] = add_rn(accC[r][c], mul_rn(cf, f0[c]));
   }
   __syncwarp();
-  if (J == 0) {
-    // f_0 enters the sums of steps 1..B-1 (b only; k = 0 is not interior)
+  // f_JB (the newest row when the block starts) enters the sums of the
+  // block's later steps; k = 0 is not part of the corrector interior
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      const double w = tb[kR * lane + r + kB];
+  for (int r = 0; r < kR; ++r) {
+    const double w1 = tb[kR * lane + r + kB];
+    const double w2 = J == 0 ? 0.0 : ta[kR * lane + r + kB];
 #pragma unroll
-      for (int c = 0; c < D; ++c) accP[r][c] = fma(w, f0[c], accP[r][c]);
+    for (int c = 0; c < D; ++c) {
+      accP[r][c] = fma(w1, fc[c], accP[r][c]);
+      accC[r][c] = fma(w2, fc[c], accC[r][c]);
     }
   }
   const double b0 = __ldg(wb), a0 = __ldg(wa);
