@@ -269,10 +269,8 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   st.err_step = first ? n : st.err_step;
   // publish (y_{n+1}, f_{n+1})
   const int ri = static_cast<int>(m1 % kRing);
-  if (lane == 0) {
-    st_pairs<D>(&S.ring[ri][0], v);
-    mbar_arrive(&S.bars[ri]);
-  }
+  if (lane == 0) st_pairs<D>(&S.ring[ri][0], v);
+  mbar_arrive_if(&S.bars[ri], lane == 0);  // predicated, keeps the warp converged
   leader_push<D, false>(S, st, m1, lane, v + D);
   // slow path: the far handoff of step n+1 was not ready when read
   if (m1 < P.N && fl != static_cast<int>(m1)) {
