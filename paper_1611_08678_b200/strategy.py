@@ -1,0 +1,87 @@
+"""Register the GPU engine as a strategy of the reference package itself.
+
+``install()`` patches a loaded ``fodeabm`` in place so that its own harness
+drives the B200 engine under the name ``"gpu"``:
+
+* ``fodeabm.bench.STRATEGIES`` gains ``"gpu"`` (bench.py:26)
+* ``fodeabm.bench._solve_once`` dispatches ``"gpu"`` to :func:`solve_gpu`
+  (bench.py:43-51), so ``run_cell`` / ``run_sweep`` time it beside serial,
+  block and reduction, with their bitwise repeat check (bench.py:80-87)
+* ``fodeabm.cli.solve_with_strategy`` does the same (cli.py:86-94) and the
+  ``--strategy`` flag accepts ``gpu`` (cli.py:171)
+
+Problems built with the reference's own rhs factories run unchanged (see
+:func:`paper_1611_08678_b200.systems.adopt_reference_rhs`).  ``uninstall()``
+restores the originals.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from .solver import STRATEGY_NAME, solve_gpu
+
+__all__ = ["install", "uninstall"]
+
+_SAVED: dict = {}
+
+
+def install(weights: str = "accurate"):
+    """Patch the imported ``fodeabm`` (bench and cli modules); returns it."""
+    fodeabm = importlib.import_module("fodeabm")
+    bench = importlib.import_module("fodeabm.bench")
+    cli = importlib.import_module("fodeabm.cli")
+    if _SAVED:
+        return fodeabm
+    _SAVED["STRATEGIES"] = bench.STRATEGIES
+    _SAVED["_solve_once"] = bench._solve_once
+    _SAVED["solve_with_strategy"] = cli.solve_with_strategy
+    _SAVED["_build_parser"] = cli._build_parser
+    orig_once = bench._solve_once
+    orig_solve = cli.solve_with_strategy
+    orig_parser = cli._build_parser
+
+    def _solve_once(problem, strategy, n_steps, workers, chunk, stats=None):
+        if strategy == STRATEGY_NAME:
+            return solve_gpu(problem, problem.grid(n_steps), weights=weights, stats=stats)
+        return orig_once(problem, strategy, n_steps, workers, chunk, stats)
+
+    def solve_with_strategy(problem, cfg):
+        if cfg.strategy == STRATEGY_NAME:
+            return solve_gpu(problem, problem.grid(cfg.n_steps), weights=weights)
+        return orig_solve(problem, cfg)
+
+    def _build_parser():
+        parser = orig_parser()
+        for action in _walk_actions(parser):
+            if action.dest == "strategy" and action.choices is not None and STRATEGY_NAME not in action.choices:
+                action.choices = (*action.choices, STRATEGY_NAME)
+        return parser
+
+    bench.STRATEGIES = (*bench.STRATEGIES, STRATEGY_NAME)
+    bench._solve_once = _solve_once
+    cli.solve_with_strategy = solve_with_strategy
+    cli._build_parser = _build_parser
+    return fodeabm
+
+
+def uninstall():
+    if not _SAVED:
+        return
+    bench = importlib.import_module("fodeabm.bench")
+    cli = importlib.import_module("fodeabm.cli")
+    bench.STRATEGIES = _SAVED["STRATEGIES"]
+    bench._solve_once = _SAVED["_solve_once"]
+    cli.solve_with_strategy = _SAVED["solve_with_strategy"]
+    cli._build_parser = _SAVED["_build_parser"]
+    _SAVED.clear()
+
+
+def _walk_actions(parser):
+    import argparse
+
+    for action in parser._actions:
+        yield action
+        if isinstance(action, argparse._SubParsersAction):
+            for sub in action.choices.values():
+                yield from _walk_actions(sub)

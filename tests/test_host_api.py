@@ -186,3 +186,46 @@ class TestReferenceInterop:
         theirs = fodeabm.rhs_hindmarsh_rose()
         for y in ((0.1, 0.2, 0.3), (-1.3, 2.0, 0.7)):
             assert ours(0.0, y) == theirs(0.0, y)
+
+
+class TestStrategyPlugin:
+    """The reference harness learns the "gpu" strategy."""
+
+    @pytest.fixture()
+    def patched(self, monkeypatch):
+        import sys
+        from pathlib import Path
+
+        src = Path("/root/reference/pkg/src")
+        if not src.exists():
+            pytest.skip("reference package not present (GPU box)")
+        sys.path.insert(0, str(src))
+        from paper_1611_08678_b200 import strategy
+
+        calls = []
+
+        def fake_solve(problem, grid, **kw):
+            calls.append((problem, grid, kw))
+            return "trajectory"
+
+        monkeypatch.setattr(strategy, "solve_gpu", fake_solve)
+        strategy.install()
+        yield calls
+        strategy.uninstall()
+
+    def test_bench_and_cli_dispatch(self, patched):
+        import fodeabm.bench as bench
+        import fodeabm.cli as cli
+
+        assert "gpu" in bench.STRATEGIES
+        problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_linear(-1.0), y0=[1.0], t_end=1.0)
+        assert bench._solve_once(problem, "gpu", 64, 1, 1024) == "trajectory"
+        assert patched[-1][1].n_steps == 64
+        cfg = cli.RunConfig(system="linear", alpha=0.5, t_max=1.0, n_steps=32, strategy="gpu")
+        assert cli.solve_with_strategy(problem, cfg) == "trajectory"
+        args = cli._build_parser().parse_args(["solve", "--system", "linear", "--alpha", "0.5", "--tmax", "1",
+                                               "--steps", "16", "--strategy", "gpu"])
+        assert args.strategy == "gpu"
+        # other strategies still reach the reference implementations
+        traj = bench._solve_once(problem, "serial", 16, 1, 1024)
+        assert traj.states.shape == (17, 1)
