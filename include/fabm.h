@@ -160,6 +160,33 @@ int fabm_plan_download_last(fabm_plan* plan, double* y_last, fabm_status* status
 int fabm_plan_stats(const fabm_plan* plan, fabm_stats* stats);
 void fabm_plan_destroy(fabm_plan* plan);
 
+/* Zero the run flags of a plan.  fabm_plan_run does this itself, except on a
+ * plan attached to peer shards: there every rank calls fabm_plan_reset, then
+ * the ranks barrier, then every rank calls fabm_plan_run. */
+int fabm_plan_reset(fabm_plan* plan, fabm_status* status);
+
+/* ---- one trajectory sharded over the GPUs of a node (BASELINE config 5) ---
+ * Replaces the reference's block-partitioned ParallelABM (parallel/block.py:
+ * 44-236 with partition.py:54-74): instead of per-step partial sums from lower
+ * workers, every GPU hosts bulk agents that own whole target blocks, so the
+ * exchange is one NVLink store of each finished target block's sums to rank 0
+ * plus the f history rows fanned out by rank 0's stepper.  Results are bitwise
+ * equal to the single-GPU run.  One process per GPU: each rank creates a plan
+ * for the same problem/grid on its own device, exports its IPC handle, the
+ * ranks all-gather the handles (rank order), and each calls attach. */
+#define FABM_IPC_HANDLE_BYTES 64
+#define FABM_MAX_SHARDS 8
+int fabm_plan_ipc_handle(fabm_plan* plan, void* handle_out, fabm_status* status);
+int fabm_plan_attach_shards(fabm_plan* plan, int n_shards, int rank, const void* handles,
+                            fabm_status* status);
+/* Close the peer mappings (every rank, then barrier, then destroy: an arena
+ * must outlive the peers' mappings of it). */
+int fabm_plan_detach_shards(fabm_plan* plan, fabm_status* status);
+/* One-GPU emulation of an n-shard run: separate per-shard f copies, control
+ * blocks and scratch on this device, agent CTA b serving shard (b-1) % n.
+ * Exercises the sharded protocol where only one GPU is available. */
+int fabm_plan_set_virtual_shards(fabm_plan* plan, int n_shards, fabm_status* status);
+
 /* ---- batch: many independent trajectories (BASELINE config 4) ----------
  * A sweep of `count` problems is `count` solve_serial calls in the reference
  * (serial.py:114-176).  problems[count] and grids[count] must share dim,

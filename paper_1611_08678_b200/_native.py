@@ -30,6 +30,9 @@ WEIGHTS_ACCURATE = 0
 WEIGHTS_FORMULA = 1
 WEIGHTS_HOST = 2
 
+IPC_HANDLE_BYTES = 64
+MAX_SHARDS = 8
+
 KIND_NAMES = {0: "none", 1: "initial", 2: "predictor", 3: "corrector"}
 
 # every symbol include/fabm.h declares (tests/test_native_abi.py checks them)
@@ -46,6 +49,11 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_download_last",
     "fabm_plan_stats",
     "fabm_plan_destroy",
+    "fabm_plan_reset",
+    "fabm_plan_ipc_handle",
+    "fabm_plan_attach_shards",
+    "fabm_plan_set_virtual_shards",
+    "fabm_plan_detach_shards",
     "fabm_solve_batch",
     "fabm_measure_dfma_peak",
 )
@@ -123,6 +131,11 @@ def _declare(lib):
         "fabm_plan_download_last": (ctypes.c_int, [plan, _DP, S]),
         "fabm_plan_stats": (ctypes.c_int, [plan, St]),
         "fabm_plan_destroy": (None, [plan]),
+        "fabm_plan_reset": (ctypes.c_int, [plan, S]),
+        "fabm_plan_ipc_handle": (ctypes.c_int, [plan, ctypes.c_void_p, S]),
+        "fabm_plan_attach_shards": (ctypes.c_int, [plan, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, S]),
+        "fabm_plan_set_virtual_shards": (ctypes.c_int, [plan, ctypes.c_int, S]),
+        "fabm_plan_detach_shards": (ctypes.c_int, [plan, S]),
         "fabm_solve_batch": (ctypes.c_int, [P, G, ctypes.c_int64, ctypes.c_int, _DP, _DP, _DP, _DP, S]),
         "fabm_measure_dfma_peak": (ctypes.c_double, [ctypes.c_int]),
     }

@@ -40,6 +40,7 @@ constexpr int kHR = 128;                // far handoff ring (handoffs run ~60 st
 constexpr int kR = 4;                   // targets per lane in a bulk tile
 constexpr int kWCols = 2 * kB / 4 + 2;  // transposed weight row length (+2 pad)
 constexpr int kMaxOwn = 256;            // owned target blocks per agent
+constexpr int kMaxShards = 8;           // GPUs of one node sharing a trajectory (config 5)
 
 enum ErrCode : int { ERR_OK = 0, ERR_NONFINITE = 1, ERR_CONFIG = 2, ERR_TIMEOUT = 3 };
 enum ErrKind : int { KIND_NONE = 0, KIND_INITIAL = 1, KIND_PREDICTOR = 2, KIND_CORRECTOR = 3 };
@@ -61,6 +62,17 @@ struct DevCtrl {
   int pad2[16];
 };
 
+// One shard = the bulk agents of one GPU.  Every shard holds a full copy of
+// the f history (the stepper's writer fans rows out to all copies over
+// NVLink), its own control block (src_done is released into it by the
+// stepper's publisher) and its own accumulator scratch for target switches.
+// Completed target sums go to shard 0's BK/ready.
+struct ShardView {
+  double* F;      // f history copy (same layout as EngineParams::F)
+  DevCtrl* ctrl;  // src_done / abort polled by this shard's agents
+  double* BK;     // accumulator scratch (spills on target switches)
+};
+
 struct EngineParams {
   long long N;             // steps
   double h, ha, ig;        // step, h^alpha, 1/Gamma(alpha+2)
@@ -80,6 +92,14 @@ struct EngineParams {
   unsigned long long timeout_ns;
   unsigned long long* trace;  // FABM_PROFILE: per block {src published, ready, staged, first need}
   int debug;               // dev experiments: 1 = leader alone (results invalid)
+  // sharding (config 5).  n_shards = 1: everything local.  my_shard >= 0: this
+  // launch hosts the agents of that shard (and the stepper if it is 0);
+  // my_shard = -1: one-GPU emulation, agent CTA b belongs to shard (b-1) % n_shards
+  int n_shards;
+  int my_shard;
+  int agent_cta_base;      // global index of this launch's first agent CTA
+  int n_agent_ctas;        // agent CTAs over all shards
+  const ShardView* shard;  // device table of n_shards views (global memory: indexed at run time)
 };
 
 __device__ __forceinline__ long long lo_of(long long m) {
@@ -99,6 +119,10 @@ __device__ __forceinline__ void ctrl_abort(DevCtrl* ctrl, int code, int kind, lo
 }
 __device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int kind, long long step, double t) {
   ctrl_abort(P.ctrl, code, kind, step, t);
+  if (P.n_shards > 1) {  // stop every shard (peer control blocks)
+    __threadfence_system();
+    for (int s = 0; s < P.n_shards; ++s) atomicExch_system(&P.shard[s].ctrl->abort, 1);
+  }
 }
 
 // ======================================================================
@@ -551,7 +575,13 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
       double* fo = P.Fc + k * D;
 #pragma unroll
       for (int c = 0; c < D; ++c) { yd[c] = yf[c]; fd[c] = yf[D + c]; fo[c] = yf[D + c]; }
+      for (int sh = 1; sh < P.n_shards; ++sh) {  // peer copies of the f history
+        double* fp = P.shard[sh].F + k * DS;
+#pragma unroll
+        for (int c = 0; c < D; ++c) fp[c] = yf[D + c];
+      }
     }
+    if (P.n_shards > 1 && ((kend + 1) % kB) == 0) __threadfence_system();
     __syncwarp();
     if (lane == 0) {
       st_volatile_smem(&S.io_done, static_cast<int>(kend + 1));
@@ -581,8 +611,13 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
     io_block = __shfl_sync(0xffffffffu, io_block, 0);
     if (io_block > published) {
       if (lane == 0) {
-        __threadfence();  // cumulative over the writer's rows (acquired above)
-        st_release_gpu(&P.ctrl->src_done, io_block);
+        if (P.n_shards == 1) {
+          __threadfence();  // cumulative over the writer's rows (acquired above)
+          st_release_gpu(&P.ctrl->src_done, io_block);
+        } else {
+          __threadfence_system();
+          for (int sh = 0; sh < P.n_shards; ++sh) st_release_sys(&P.shard[sh].ctrl->src_done, io_block);
+        }
 #ifdef FABM_PROFILE
         if (P.trace)
           for (int q = published; q < io_block; ++q) P.trace[4 * q + 0] = global_ns();
@@ -597,7 +632,7 @@ __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lan
     if (next_stage < nb && ld_volatile_smem(&S.io_done) - 1 >= static_cast<long long>(next_stage - 1) * kB) {
       int rdy = 1;
       if (next_stage >= kL) {
-        if (lane == 0) rdy = ld_acquire_gpu(&P.ready[next_stage]);
+        if (lane == 0) rdy = P.n_shards == 1 ? ld_acquire_gpu(&P.ready[next_stage]) : ld_acquire_sys(&P.ready[next_stage]);
         rdy = __shfl_sync(0xffffffffu, rdy, 0);
       }
       if (rdy) {
@@ -682,24 +717,24 @@ struct AgentSmem {
 };
 
 template <int D>
-__device__ __forceinline__ void agent_store_acc(const EngineParams& P, int J, int lane,
+__device__ __forceinline__ void agent_store_acc(double* BK, int J, int lane,
                                                 const double (&accP)[kR][D], const double (&accC)[kR][D]) {
   constexpr int DS = Stride<D>::value;
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
-    double* dst = P.BK + (static_cast<long long>(J) * kB + kR * lane + r) * 2 * DS;
+    double* dst = BK + (static_cast<long long>(J) * kB + kR * lane + r) * 2 * DS;
 #pragma unroll
     for (int c = 0; c < D; ++c) { dst[c] = accP[r][c]; dst[DS + c] = accC[r][c]; }
   }
 }
 
 template <int D>
-__device__ __forceinline__ void agent_load_acc(const EngineParams& P, int J, int lane,
+__device__ __forceinline__ void agent_load_acc(const double* BK, int J, int lane,
                                                double (&accP)[kR][D], double (&accC)[kR][D]) {
   constexpr int DS = Stride<D>::value;
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
-    const double* src = P.BK + (static_cast<long long>(J) * kB + kR * lane + r) * 2 * DS;
+    const double* src = BK + (static_cast<long long>(J) * kB + kR * lane + r) * 2 * DS;
 #pragma unroll
     for (int c = 0; c < D; ++c) { accP[r][c] = __ldcg(src + c); accC[r][c] = __ldcg(src + DS + c); }
   }
@@ -779,7 +814,7 @@ __device__ __forceinline__ int owned_count(int agent, int nA, int n_targets) {
 }
 
 template <int D>
-__device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int lane) {
+__device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int lane, const ShardView& sv) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
   if (agent >= n_targets) return;
@@ -805,7 +840,15 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
 #endif
   while (done < nown) {
     int M = 0, ab = 0;
-    if (lane == 0) { M = ld_acquire_gpu(&P.ctrl->src_done); ab = ld_relaxed_gpu(&P.ctrl->abort); }
+    if (lane == 0) {
+      if (P.n_shards == 1) {
+        M = ld_acquire_gpu(&sv.ctrl->src_done);
+        ab = ld_relaxed_gpu(&sv.ctrl->abort);
+      } else {
+        M = ld_acquire_sys(&sv.ctrl->src_done);
+        ab = ld_relaxed_sys(&sv.ctrl->abort);
+      }
+    }
     M = __shfl_sync(0xffffffffu, M, 0);
     ab = __shfl_sync(0xffffffffu, ab, 0);
     if (ab) return;
@@ -836,9 +879,9 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     last_progress = global_ns();
     const int J = owned_target(agent, best, nA);
     if (cur != best) {
-      if (cur >= 0) agent_store_acc<D>(P, owned_target(agent, cur, nA), lane, accP, accC);
+      if (cur >= 0) agent_store_acc<D>(sv.BK, owned_target(agent, cur, nA), lane, accP, accC);
       if (A.own_next[best] > 0) {
-        agent_load_acc<D>(P, J, lane, accP, accC);
+        agent_load_acc<D>(sv.BK, J, lane, accP, accC);
       } else {
 #pragma unroll
         for (int r = 0; r < kR; ++r)
@@ -852,8 +895,8 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     int nx = A.own_next[best];
     while (nx < lim) {
       int M2 = 0;
-      if (lane == 0) M2 = ld_relaxed_gpu(&P.ctrl->src_done);
-      agent_tile<D>(P.wb, P.wa, P.F, A, nx, J, lane, accP, accC);
+      if (lane == 0) M2 = P.n_shards == 1 ? ld_relaxed_gpu(&sv.ctrl->src_done) : ld_relaxed_sys(&sv.ctrl->src_done);
+      agent_tile<D>(P.wb, P.wa, sv.F, A, nx, J, lane, accP, accC);
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
@@ -864,10 +907,16 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     if (lane == 0) A.own_next[best] = nx;
     __syncwarp();
     if (nx == J - kL + 1) {
-      agent_store_acc<D>(P, J, lane, accP, accC);
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_release_gpu(&P.ready[J], 1);
+      agent_store_acc<D>(P.BK, J, lane, accP, accC);  // shard 0's BK (peer memory on other GPUs)
+      if (P.n_shards == 1) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(&P.ready[J], 1);
+      } else {
+        __threadfence_system();
+        __syncwarp();
+        if (lane == 0) st_release_sys(&P.ready[J], 1);
+      }
 #ifdef FABM_PROFILE
       if (P.trace && lane == 0) P.trace[4 * J + 1] = global_ns();
 #endif
@@ -875,7 +924,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
       ++done;
     }
   }
-  if (lane == 0) atomicAdd(&P.ctrl->bulk_tiles, tiles);
+  if (lane == 0) atomicAdd(&sv.ctrl->bulk_tiles, tiles);
 #ifdef FABM_PROFILE
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[4]), (unsigned long long)c_tile);
@@ -890,14 +939,17 @@ template <int SYS, int D>
 __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   if (blockIdx.x == 0) {
-    stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
+    if (P.my_shard <= 0) stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
   } else {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     AgentSmem* A = reinterpret_cast<AgentSmem*>(smem_raw) + warp;
-    // agents are dealt warp-major across CTAs so every SM hosts a mix of
-    // light and heavy owners: when light agents finish, the heavy ones on the
-    // same SM inherit its FP64 throughput
-    bulk_agent<D>(P, *A, warp * (gridDim.x - 1) + (blockIdx.x - 1), lane);
+    const int lcta = blockIdx.x - 1;
+    const int sh = P.my_shard >= 0 ? P.my_shard : lcta % P.n_shards;
+    // agents are dealt warp-major across CTAs (of all shards) so every SM
+    // hosts a mix of light and heavy owners: when light agents finish, the
+    // heavy ones on the same SM inherit its FP64 throughput
+    const ShardView sv = P.shard[sh];
+    bulk_agent<D>(P, *A, warp * P.n_agent_ctas + P.agent_cta_base + lcta, lane, sv);
   }
 }
 

@@ -175,11 +175,27 @@ struct fabm_plan {
   double* wc = nullptr;
   double* y0 = nullptr;
   double* Y = nullptr;
-  double* F = nullptr;
   double* Fc = nullptr;
+  // the shard arena: {ctrl, ready, F, BK} in one allocation so that one CUDA
+  // IPC handle exposes it to the peer GPUs of a sharded run (config 5)
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  size_t off_ready = 0, off_F = 0, off_BK = 0;
+  double* F = nullptr;
   double* BK = nullptr;
   int* ready = nullptr;
   DevCtrl* ctrl = nullptr;
+  // sharding: n_shards = 1 (default), real (one process per GPU, peers opened
+  // from IPC handles) or virtual (one-GPU emulation with local arenas)
+  int n_shards = 1;
+  int rank = 0;
+  bool virt = false;
+  bool armed = false;          // real sharded runs: flags reset and not yet run
+  int agent_ctas_per_shard = 0;
+  std::vector<char*> peer;     // arena base of every shard (peer[rank] = arena)
+  std::vector<char*> opened;   // IPC mappings to close
+  std::vector<char*> virt_arenas;
+  ShardView* shard_tab = nullptr;  // device copy of the per-shard views
   bool weights_ready = false;
   int weights_mode = FABM_WEIGHTS_ACCURATE;
   int bulk_ctas = 0;
@@ -192,8 +208,10 @@ static void plan_free(fabm_plan* p) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
-  for (void* ptr : {(void*)p->wb, (void*)p->wa, (void*)p->wc, (void*)p->y0, (void*)p->Y, (void*)p->F,
-                    (void*)p->Fc, (void*)p->BK, (void*)p->ready, (void*)p->ctrl})
+  for (char* m : p->opened) cudaIpcCloseMemHandle(m);
+  for (char* m : p->virt_arenas) cudaFree(m);
+  for (void* ptr : {(void*)p->wb, (void*)p->wa, (void*)p->wc, (void*)p->y0, (void*)p->Y, (void*)p->Fc,
+                    (void*)p->arena, (void*)p->shard_tab})
     if (ptr) cudaFree(ptr);
   for (auto& e : p->ev)
     if (e) cudaEventDestroy(e);
@@ -269,13 +287,23 @@ fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid_i
   if ((e = cudaMalloc(&p->wc, wbytes)) != cudaSuccess) return fail("malloc c", e);
   if ((e = cudaMalloc(&p->y0, sizeof(double) * FABM_MAX_DIM)) != cudaSuccess) return fail("malloc y0", e);
   if ((e = cudaMalloc(&p->Y, sizeof(double) * (p->N + 1) * problem->dim)) != cudaSuccess) return fail("malloc Y", e);
-  if ((e = cudaMalloc(&p->F, sizeof(double) * fl)) != cudaSuccess) return fail("malloc F", e);
   if ((e = cudaMalloc(&p->Fc, sizeof(double) * (p->N + 1) * problem->dim)) != cudaSuccess) return fail("malloc Fc", e);
-  if ((e = cudaMalloc(&p->BK, sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds)) != cudaSuccess)
-    return fail("malloc BK", e);
-  if ((e = cudaMalloc(&p->ready, sizeof(int) * (p->nb + 1))) != cudaSuccess) return fail("malloc ready", e);
-  if ((e = cudaMalloc(&p->ctrl, sizeof(DevCtrl))) != cudaSuccess) return fail("malloc ctrl", e);
-  cudaMemsetAsync(p->F, 0, sizeof(double) * fl, p->stream);
+  {
+    auto up = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    p->off_ready = up(sizeof(DevCtrl));
+    p->off_F = p->off_ready + up(sizeof(int) * (p->nb + 1));
+    p->off_BK = p->off_F + up(sizeof(double) * fl);
+    p->arena_bytes = p->off_BK + up(sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds);
+  }
+  if ((e = cudaMalloc(&p->arena, p->arena_bytes)) != cudaSuccess) return fail("malloc arena", e);
+  if ((e = cudaMalloc(&p->shard_tab, sizeof(ShardView) * kMaxShards)) != cudaSuccess) return fail("malloc shards", e);
+  p->ctrl = reinterpret_cast<DevCtrl*>(p->arena);
+  p->ready = reinterpret_cast<int*>(p->arena + p->off_ready);
+  p->F = reinterpret_cast<double*>(p->arena + p->off_F);
+  p->BK = reinterpret_cast<double*>(p->arena + p->off_BK);
+  p->peer.assign(1, p->arena);
+  p->agent_ctas_per_shard = p->bulk_ctas;
+  cudaMemsetAsync(p->arena, 0, p->arena_bytes, p->stream);
   cudaMemsetAsync(p->wb, 0, wbytes, p->stream);
   cudaMemsetAsync(p->wa, 0, wbytes, p->stream);
   cudaMemsetAsync(p->wc, 0, wbytes, p->stream);
@@ -347,8 +375,17 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     int rc = fabm_plan_set_weights(p, FABM_WEIGHTS_ACCURATE, nullptr, nullptr, nullptr, status);
     if (rc != FABM_OK) return rc;
   }
-  CUDA_TRY(cudaMemsetAsync(p->ctrl, 0, sizeof(DevCtrl), p->stream));
-  CUDA_TRY(cudaMemsetAsync(p->ready, 0, sizeof(int) * (p->nb + 1), p->stream));
+  const bool real_shards = p->n_shards > 1 && !p->virt;
+  if (real_shards) {
+    if (!p->armed) {
+      set_status(status, FABM_ERR_CONFIG, "sharded plan: call fabm_plan_reset on every rank, then barrier, then run");
+      return FABM_ERR_CONFIG;
+    }
+    p->armed = false;
+  } else {
+    int rc = fabm_plan_reset(p, status);
+    if (rc != FABM_OK) return rc;
+  }
   EngineParams P{};
   P.N = p->N;
   P.h = p->grid.h;
@@ -366,7 +403,33 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   P.ctrl = p->ctrl;
   std::memcpy(P.params, p->prob.params, sizeof(P.params));
   P.nb = p->nb;
-  P.n_agents = p->bulk_ctas * kWarps;
+  P.n_shards = p->n_shards;
+  {
+    ShardView tab[kMaxShards] = {};
+    for (int sh = 0; sh < p->n_shards; ++sh) {
+      char* base = p->peer[sh];
+      tab[sh].ctrl = reinterpret_cast<DevCtrl*>(base);
+      tab[sh].F = reinterpret_cast<double*>(base + p->off_F);
+      tab[sh].BK = reinterpret_cast<double*>(base + p->off_BK);
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->shard_tab, tab, sizeof(tab), cudaMemcpyHostToDevice, p->stream));
+    P.shard = p->shard_tab;
+  }
+  int grid = 1 + p->bulk_ctas;
+  if (real_shards) {
+    // completed targets land in shard 0's accumulators; the stepper lives there
+    P.BK = reinterpret_cast<double*>(p->peer[0] + p->off_BK);
+    P.ready = reinterpret_cast<int*>(p->peer[0] + p->off_ready);
+    P.my_shard = p->rank;
+    P.agent_cta_base = p->rank * p->agent_ctas_per_shard;
+    P.n_agent_ctas = p->n_shards * p->agent_ctas_per_shard;
+    grid = 1 + p->agent_ctas_per_shard;
+  } else {
+    P.my_shard = p->virt ? -1 : 0;
+    P.agent_cta_base = 0;
+    P.n_agent_ctas = p->bulk_ctas;
+  }
+  P.n_agents = P.n_agent_ctas * kWarps;
 #ifdef FABM_PROFILE
   if (g_trace_n < 4 * (p->nb + 1)) {
     if (g_trace) cudaFree(g_trace);
@@ -379,7 +442,6 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   const double tmo = timeout_s > 0 ? timeout_s : 60.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   if (const char* dbg = getenv("FABM_DEBUG_MODE")) P.debug = atoi(dbg);
-  const int grid = 1 + p->bulk_ctas;
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
   CUDA_TRY(p->launch(P, grid, p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[1], p->stream));
@@ -388,6 +450,23 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]);
   DevCtrl h{};
   CUDA_TRY(cudaMemcpy(&h, p->ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost));
+  if (p->virt) {  // emulated shards: their agents count tiles / raise errors in their own blocks
+    for (int sh = 1; sh < p->n_shards; ++sh) {
+      DevCtrl v{};
+      CUDA_TRY(cudaMemcpy(&v, p->peer[sh], sizeof(DevCtrl), cudaMemcpyDeviceToHost));
+      h.bulk_tiles += v.bulk_tiles;
+      if (h.err_code == ERR_OK && v.err_code != ERR_OK) {
+        h.err_code = v.err_code;
+        h.err_kind = v.err_kind;
+        h.err_step = v.err_step;
+        h.err_t = v.err_t;
+      }
+    }
+  }
+  if (h.err_code == ERR_OK && h.abort) {  // stopped by a peer shard (its watchdog or its error)
+    h.err_code = ERR_TIMEOUT;
+    h.err_step = -3;
+  }
   p->stats.kernel_ms = ms;
   p->stats.steps = p->N;
   p->stats.history_fma = static_cast<int64_t>(p->prob.dim) * p->N * p->N;
@@ -401,13 +480,124 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
       status->kind = h.err_kind;
       status->step = h.err_step;
       status->t = h.err_t;
-      if (h.err_code == ERR_TIMEOUT)
+      if (h.err_code == ERR_TIMEOUT && h.err_step == -3)
+        snprintf(status->message, sizeof(status->message), "aborted by a peer shard");
+      else if (h.err_code == ERR_TIMEOUT)
         snprintf(status->message, sizeof(status->message), "device watchdog expired (no progress for %.1f s)", tmo);
       else
         snprintf(status->message, sizeof(status->message), "rhs returned a non-finite value");
     }
     return h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;
   }
+  return FABM_OK;
+}
+
+int fabm_plan_reset(fabm_plan* p, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaMemsetAsync(p->ctrl, 0, sizeof(DevCtrl), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->ready, 0, sizeof(int) * (p->nb + 1), p->stream));
+  for (char* va : p->virt_arenas) CUDA_TRY(cudaMemsetAsync(va, 0, sizeof(DevCtrl), p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->armed = true;
+  return FABM_OK;
+}
+
+// agent CTAs per shard for a sharded run (every GPU hosts the same count)
+static int shard_ctas(const fabm_plan* p, int n_shards) {
+  const int n_targets = p->nb - kL;
+  if (n_targets <= 0) return 1;
+  const int want = (n_targets + kWarps - 1) / kWarps;
+  return std::max(1, std::min(p->num_sms - 1, (want + n_shards - 1) / n_shards));
+}
+
+int fabm_plan_set_virtual_shards(fabm_plan* p, int n_shards, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if (n_shards < 1 || n_shards > kMaxShards || (p->n_shards > 1 && !p->virt)) {
+    set_status(status, FABM_ERR_CONFIG, "virtual shards: need 1..%d and a plan not attached to peers", kMaxShards);
+    return FABM_ERR_CONFIG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  for (char* m : p->virt_arenas) cudaFree(m);
+  p->virt_arenas.clear();
+  p->peer.assign(1, p->arena);
+  for (int sh = 1; sh < n_shards; ++sh) {
+    char* m = nullptr;
+    CUDA_TRY(cudaMalloc(&m, p->arena_bytes));
+    CUDA_TRY(cudaMemsetAsync(m, 0, p->arena_bytes, p->stream));
+    p->virt_arenas.push_back(m);
+    p->peer.push_back(m);
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->n_shards = n_shards;
+  p->virt = n_shards > 1;
+  return FABM_OK;
+}
+
+int fabm_plan_ipc_handle(fabm_plan* p, void* handle_out, fabm_status* status) {
+  clear_status(status);
+  if (!p || !handle_out) { set_status(status, FABM_ERR_CONFIG, "null plan/output"); return FABM_ERR_CONFIG; }
+  static_assert(sizeof(cudaIpcMemHandle_t) == FABM_IPC_HANDLE_BYTES, "IPC handle size");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p->arena));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return FABM_OK;
+}
+
+int fabm_plan_attach_shards(fabm_plan* p, int n_shards, int rank, const void* handles, fabm_status* status) {
+  clear_status(status);
+  if (!p || !handles) { set_status(status, FABM_ERR_CONFIG, "null plan/handles"); return FABM_ERR_CONFIG; }
+  if (n_shards < 1 || n_shards > kMaxShards || rank < 0 || rank >= n_shards || p->virt) {
+    set_status(status, FABM_ERR_CONFIG, "attach: need 1 <= n_shards <= %d, 0 <= rank < n_shards", kMaxShards);
+    return FABM_ERR_CONFIG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  for (char* m : p->opened) cudaIpcCloseMemHandle(m);
+  p->opened.clear();
+  p->peer.assign(n_shards, nullptr);
+  const auto* hb = static_cast<const unsigned char*>(handles);
+  for (int sh = 0; sh < n_shards; ++sh) {
+    if (sh == rank) { p->peer[sh] = p->arena; continue; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + static_cast<size_t>(sh) * FABM_IPC_HANDLE_BYTES, sizeof(h));
+    void* m = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&m, h, cudaIpcMemLazyEnablePeerAccess));
+    p->opened.push_back(static_cast<char*>(m));
+    p->peer[sh] = static_cast<char*>(m);
+  }
+  p->n_shards = n_shards;
+  p->rank = rank;
+  p->armed = false;
+  p->agent_ctas_per_shard = shard_ctas(p, n_shards);
+  const int n_agents = n_shards * p->agent_ctas_per_shard * kWarps;
+  const int n_targets = p->nb - kL;
+  if (n_targets > 0 && (n_targets + n_agents - 1) / n_agents > kMaxOwn) {
+    set_status(status, FABM_ERR_CONFIG, "n_steps=%lld exceeds the engine capacity", p->N);
+    return FABM_ERR_CONFIG;
+  }
+  p->stats.bulk_ctas = p->agent_ctas_per_shard;
+  return FABM_OK;
+}
+
+int fabm_plan_detach_shards(fabm_plan* p, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  for (char* m : p->opened) CUDA_TRY(cudaIpcCloseMemHandle(m));
+  p->opened.clear();
+  for (char* m : p->virt_arenas) cudaFree(m);
+  p->virt_arenas.clear();
+  p->peer.assign(1, p->arena);
+  p->n_shards = 1;
+  p->rank = 0;
+  p->virt = false;
+  p->armed = false;
+  p->agent_ctas_per_shard = p->bulk_ctas;
+  p->stats.bulk_ctas = p->bulk_ctas;
   return FABM_OK;
 }
 

@@ -1,17 +1,26 @@
 """Multi-GPU plumbing: one process per GPU over torch.distributed (NCCL on the
 B200 box, gloo for the CPU tests).
 
-Only the batched sweep shards (BASELINE config 4): trajectories are
-independent, so each rank integrates a contiguous slice with no data-path
-collective, and the final states are all-gathered once.  The single headline
-trajectory does not shard in this round (replicas only).
+Two sharded paths:
+
+* the batched sweep (BASELINE config 4): trajectories are independent, so each
+  rank integrates a contiguous slice with no data-path collective, and the
+  final states are all-gathered once (:func:`solve_batch_distributed`);
+* one long trajectory (config 5, :func:`solve_sharded`): every rank hosts
+  bulk agents of the same engine; rank 0 also runs the stepper.  The ranks
+  exchange CUDA IPC handles of their shard arenas once, then the kernels talk
+  over NVLink (f rows out of rank 0, finished target-block sums into rank 0).
+  This replaces the reference's block-partitioned ParallelABM
+  (parallel/block.py:44-236), whose lower workers send per-step partial sums
+  to the owner; here each future block costs one store, and the result is
+  bitwise equal to the single-GPU solve.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["shard_bounds", "gather_rows", "solve_batch_distributed"]
+__all__ = ["shard_bounds", "gather_rows", "solve_batch_distributed", "solve_sharded"]
 
 
 def shard_bounds(count: int, world: int, rank: int) -> tuple[int, int]:
@@ -63,3 +72,116 @@ def solve_batch_distributed(problems, grid, *, solver=None, device: int | None =
         kwargs["device"] = device
     res = solver(problems[lo:hi], grid, **kwargs)
     return gather_rows(res.y_last, len(problems), world, rank, group), res
+
+
+def _error_record(exc):
+    """A picklable summary of a solve error (exceptions with keyword-only
+    state do not survive all_gather_object)."""
+    from .core import SolverStepError, StrategyTimeoutError
+
+    if exc is None:
+        return None
+    if isinstance(exc, SolverStepError):
+        return ("step", str(exc), exc.step, exc.t)
+    if isinstance(exc, StrategyTimeoutError):
+        return ("timeout", str(exc), None, None)
+    if isinstance(exc, ValueError):
+        return ("value", str(exc), None, None)
+    return ("runtime", f"{type(exc).__name__}: {exc}", None, None)
+
+
+def _raise_record(rec, rank):
+    from .core import SolverStepError, StrategyTimeoutError
+
+    kind, msg, step, t = rec
+    if kind == "step":
+        raise SolverStepError("rhs returned a non-finite value", step=step, t=t)
+    if kind == "timeout":
+        raise StrategyTimeoutError(f"rank {rank}: {msg}")
+    if kind == "value":
+        raise ValueError(msg)
+    raise RuntimeError(f"rank {rank}: {msg}")
+
+
+def first_error(records):
+    """The error every rank raises after a sharded solve: the stepper's (rank
+    0) unless it was only the echo of a peer's abort, else the lowest rank's."""
+    recs = [(r, rec) for r, rec in enumerate(records) if rec is not None]
+    if not recs:
+        return None
+    for r, rec in recs:
+        if "aborted by a peer shard" not in rec[1]:
+            return r, rec
+    return recs[0]
+
+
+def solve_sharded(problem, grid, *, weights="accurate", device: int | None = None, timeout_s: float | None = None,
+                  group=None, plan_cls=None):
+    """Integrate ONE trajectory with its history sharded over the ranks of
+    ``group`` (one process per GPU).  Collective: every rank calls it with the
+    same problem and grid.  Rank 0 returns the :class:`Trajectory`, the others
+    ``None``; an error on any rank raises the same exception on every rank.
+    """
+    import os
+
+    import torch.distributed as dist
+
+    from .solver import DEFAULT_TIMEOUT_S, GpuPlan, solve_gpu
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    timeout_s = DEFAULT_TIMEOUT_S if timeout_s is None else timeout_s
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", rank))
+    if world == 1 and plan_cls is None:
+        return solve_gpu(problem, grid, weights=weights, device=device, timeout_s=timeout_s)
+    if plan_cls is None:
+        plan_cls = GpuPlan
+    if not grid.spans(problem.t_end):
+        raise ValueError(f"grid (h={grid.h!r}, N={grid.n_steps}) does not span t_end={problem.t_end!r}")
+    problem.eval_rhs0()
+    err = None
+    plan = None
+    try:
+        plan = plan_cls(problem, grid, weights=weights, device=device)
+        plan.set_y0(problem.y0)
+        handle = plan.ipc_handle()
+    except Exception as exc:  # keep the collective sequence aligned across ranks
+        err, handle = exc, None
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    if err is None and any(h is None for h in handles):
+        err = RuntimeError("a peer rank failed to create its shard")
+    if err is None:
+        try:
+            plan.attach_shards(world, rank, b"".join(handles))
+            plan.reset()
+        except Exception as exc:
+            err = exc
+    oks = [None] * world
+    dist.all_gather_object(oks, err is None, group=group)  # doubles as the pre-launch barrier
+    if err is None and not all(oks):
+        err = RuntimeError("a peer rank failed to attach its shard")
+    if err is None:
+        try:
+            plan.run(timeout_s)
+        except Exception as exc:
+            err = exc
+    records = [None] * world
+    dist.all_gather_object(records, _error_record(err), group=group)
+    picked = first_error(records)
+    traj = None
+    if picked is None and rank == 0:
+        traj = plan.download()
+    # an arena must outlive the peers' mappings of it: detach, barrier, free
+    if plan is not None:
+        try:
+            plan.detach_shards()
+        except Exception:
+            pass
+    dist.barrier(group=group)
+    if plan is not None:
+        plan.close()
+    if picked is not None:
+        _raise_record(picked[1], picked[0])
+    return traj

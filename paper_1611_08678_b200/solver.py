@@ -18,6 +18,7 @@ Weights (the ``precompute_weights`` seam, serial.py:130):
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 from collections import OrderedDict
@@ -143,6 +144,41 @@ class GpuPlan:
         y0 = np.ascontiguousarray(np.asarray(y0, dtype=np.float64).reshape(-1))
         st = nat.Status()
         if self._lib.fabm_plan_set_y0(self._h, nat.dptr(y0), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    # -- sharding (config 5) ------------------------------
+    def ipc_handle(self) -> bytes:
+        """CUDA IPC handle of this plan's shard arena (exchanged between ranks)."""
+        buf = ctypes.create_string_buffer(nat.IPC_HANDLE_BYTES)
+        st = nat.Status()
+        if self._lib.fabm_plan_ipc_handle(self._h, buf, ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+        return buf.raw
+
+    def attach_shards(self, n_shards: int, rank: int, handles: bytes):
+        """Map the arenas of all ranks (handles in rank order, IPC_HANDLE_BYTES each)."""
+        if len(handles) != n_shards * nat.IPC_HANDLE_BYTES:
+            raise ValueError(f"expected {n_shards} IPC handles")
+        st = nat.Status()
+        if self._lib.fabm_plan_attach_shards(self._h, int(n_shards), int(rank), handles, ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    def set_virtual_shards(self, n_shards: int):
+        """Emulate an n-shard run on this one GPU (same protocol, local buffers)."""
+        st = nat.Status()
+        if self._lib.fabm_plan_set_virtual_shards(self._h, int(n_shards), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    def detach_shards(self):
+        """Close the peer mappings and return to a single-GPU plan."""
+        st = nat.Status()
+        if self._lib.fabm_plan_detach_shards(self._h, ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    def reset(self):
+        """Zero the run flags (sharded plans: on every rank, before the barrier)."""
+        st = nat.Status()
+        if self._lib.fabm_plan_reset(self._h, ctypes_ref(st)) != nat.FABM_OK:
             _raise_status(st)
 
     # -- execution -----------------------------------------------------
