@@ -99,6 +99,14 @@ __device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
       "r"(static_cast<uint32_t>(pred))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_if_u32(uint32_t bar, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "@p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
+      "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
 // non-blocking probe of phase completion, acquire semantics on success
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;

@@ -30,6 +30,8 @@ constexpr int kSlots = kL * kB;         // 512 far-window slots
 constexpr int kChunk = 32;              // near window: k in [32(c-1), m-1] for m in chunk c (leader warp)
 constexpr int kGFar = 2 * kChunk + 1;   // sizing of the zero-padded weight tables
 constexpr int kHelperWarps = 8;         // warps 1,2,3,5,6,7,9,10 (SMSPs 1-3)
+constexpr int kWriterWarp = 13;         // SMSP 1
+constexpr int kPublisherWarp = 14;      // SMSP 2
 constexpr int kSlotsPerThread = kSlots / (kHelperWarps * 32);  // 2
 constexpr int kBatch = 8;               // publishes consumed per helper wake-up
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
@@ -226,21 +228,23 @@ struct LeaderState {
   long long err_step;
 };
 
-// near sums of step m1 (owner lane -> all lanes via smem) and its far handoff
-template <int D>
-__device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st, long long m1, int lane,
-                                             double* nr, double* fr) {
-  if ((m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation A <- B, B <- 0
+// near sums of step m1 (owner lane -> all lanes via smem) and its far handoff.
+// ROT: a chunk rotation is possible at this step (the fast block path knows
+// statically where the 32-step chunk boundaries can fall).
+template <int D, bool ROT>
+__device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st, int m1, int lane, double* nr,
+                                             double* fr, bool acquire_flag) {
+  if (ROT && (m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation A <- B, B <- 0
 #pragma unroll
     for (int c = 0; c < 2 * D; ++c) { st.accA[c] = st.accB[c]; st.accB[c] = 0.0; }
     st.cA += 1;
   }
-  const int owner = static_cast<int>(m1 & (kChunk - 1));
+  const int owner = m1 & (kChunk - 1);
   double* xb = &S.xfer[m1 & 1][0];
   if (lane == owner) st_pairs<D>(xb, st.accA);
   __syncwarp();
-  const int slot = static_cast<int>(m1 % kHR);
-  const int fl = ld_acquire_cta_smem(&S.hflag[slot]);
+  const int slot = m1 & (kHR - 1);
+  const int fl = acquire_flag ? ld_acquire_cta_smem(&S.hflag[slot]) : m1;
   ld_pairs<D>(xb, nr);
   ld_pairs<D>(&S.hbuf[slot][0], fr);
   return fl;
@@ -248,35 +252,54 @@ __device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st,
 
 // push f_k (k = m1, just computed) into the near sums of A and B; the padded
 // weight tables give 0 for steps already consumed (j <= 0)
-template <int D, bool K0>
-__device__ __forceinline__ void leader_push(const StepperSmem& S, LeaderState<D>& st, long long m1, int lane,
-                                            const double* fk) {
-  const int k = static_cast<int>(m1);
-  const int jA = st.cA * kChunk + lane - k;  // -31..31
-  const int jB = jA + kChunk;                // 1..63
-  const double wbA = S.tb[jA + 2 * kChunk - 1], wbB = S.tb[jB + 2 * kChunk - 1];
-  const double waA = K0 ? 0.0 : S.ta[jA + 2 * kChunk - 1];  // corrector interior excludes k = 0
-  const double waB = K0 ? 0.0 : S.ta[jB + 2 * kChunk - 1];
+struct PushW {
+  double bA, bB, aA, aB;
+};
+template <bool K0>
+__device__ __forceinline__ PushW leader_push_weights(const StepperSmem& S, int cA, int m1, int lane) {
+  const int jA = cA * kChunk + lane - m1;  // -31..31
+  const int jB = jA + kChunk;              // 1..63
+  PushW w;
+  w.bA = S.tb[jA + 2 * kChunk - 1];
+  w.bB = S.tb[jB + 2 * kChunk - 1];
+  w.aA = K0 ? 0.0 : S.ta[jA + 2 * kChunk - 1];  // corrector interior excludes k = 0
+  w.aB = K0 ? 0.0 : S.ta[jB + 2 * kChunk - 1];
+  return w;
+}
+template <int D>
+__device__ __forceinline__ void leader_push(LeaderState<D>& st, const PushW& w, const double* fk) {
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    st.accA[c] = fma(wbA, fk[c], st.accA[c]);
-    st.accA[D + c] = fma(waA, fk[c], st.accA[D + c]);
-    st.accB[c] = fma(wbB, fk[c], st.accB[c]);
-    st.accB[D + c] = fma(waB, fk[c], st.accB[D + c]);
+    st.accA[c] = fma(w.bA, fk[c], st.accA[c]);
+    st.accA[D + c] = fma(w.aA, fk[c], st.accA[D + c]);
+    st.accB[c] = fma(w.bB, fk[c], st.accB[c]);
+    st.accB[D + c] = fma(w.aB, fk[c], st.accB[D + c]);
   }
 }
 
-// One step n of the sequential chain (serial.py:150-170).
-template <int SYS, int D>
+// One step n of the sequential chain (serial.py:150-170).  Source order is
+// the issue order the in-order warp needs: everything that does not depend on
+// this step's f (the gather of step n+1, its pre-sums, the push weights) is
+// issued before the chain so it completes under the chain's FP64 latencies.
+//   FAST: the caller verified every far handoff of the enclosing 8-step
+//         block (leader_block_ready) -- no per-step flag test or slow path;
+//   ROT:  a chunk rotation can happen at this step.
+template <int SYS, int D, bool FAST, bool ROT>
 __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, LeaderState<D>& st,
-                                            double b0, double a0, long long n, int lane,
+                                            double b0, double a0e, int n, int lane, uint32_t bars_u32,
                                             unsigned long long& waited) {
-  const long long m1 = n + 1;
+  const int m1 = n + 1;
   double nr[2 * D], fr[2 * D];
-  const int fl = leader_gather<D>(S, st, m1, lane, nr, fr);
+  const int fl = leader_gather<D, ROT>(S, st, m1, lane, nr, fr, !FAST);
+  const PushW pw = leader_push_weights<false>(S, st.cA, m1, lane);
+  double nxP[D], nxC[D];  // pre-sums of step n+1 = near + far
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    nxP[c] = nr[c] + fr[c];
+    nxC[c] = nr[D + c] + fr[D + c];
+  }
   const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
   const double ha = P.ha;
-  const double a0e = n >= 1 ? a0 : 0.0;  // corrector interior starts at k = 1
   double yP[D], fP[D], v[2 * D];
 #pragma unroll
   for (int c = 0; c < D; ++c) yP[c] = add_rn(mul_rn(fma(b0, st.fc[c], st.preP[c]), ha), st.y0[c]);
@@ -285,35 +308,57 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   for (int c = 0; c < D; ++c)  // ((c_n f0 + C_n) + fP/G2) * h^a + y0, serial.py:160-165
     v[c] = add_rn(mul_rn(add_rn(fma(a0e, st.fc[c], st.preC[c]), mul_rn(P.ig, fP[c])), ha), st.y0[c]);
   Rhs<SYS, D>::eval(t1, v, v + D, P.params);
+  // publish (y_{n+1}, f_{n+1})
+  const int ri = m1 & (kRing - 1);
+  if (lane == 0) st_pairs<D>(&S.ring[ri][0], v);
+  mbar_arrive_if_u32(bars_u32 + 8u * static_cast<uint32_t>(ri), lane == 0);  // predicated: warp stays converged
+  leader_push<D>(st, pw, v + D);
+#pragma unroll
+  for (int c = 0; c < D; ++c) st.fc[c] = v[D + c];
   // first non-finite rhs output: predictor before corrector (serial.py:157,167)
   const bool bp = any_nonfinite<D>(fP), bc = any_nonfinite<D>(v + D);
   const int kind = bp ? KIND_PREDICTOR : (bc ? KIND_CORRECTOR : KIND_NONE);
   const bool first = (kind != KIND_NONE) & (st.err_kind == KIND_NONE);
   st.err_kind = first ? kind : st.err_kind;
   st.err_step = first ? n : st.err_step;
-  // publish (y_{n+1}, f_{n+1})
-  const int ri = static_cast<int>(m1 % kRing);
-  if (lane == 0) st_pairs<D>(&S.ring[ri][0], v);
-  mbar_arrive_if(&S.bars[ri], lane == 0);  // predicated, keeps the warp converged
-  leader_push<D, false>(S, st, m1, lane, v + D);
   // slow path: the far handoff of step n+1 was not ready when read
-  if (m1 < P.N && fl != static_cast<int>(m1)) {
+  if (!FAST && m1 < P.N && fl != m1) {
     if (!leader_wait_handoff(P, S, m1, waited)) return false;
-    ld_pairs<D>(&S.hbuf[m1 % kHR][0], fr);
+    ld_pairs<D>(&S.hbuf[m1 & (kHR - 1)][0], fr);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      nxP[c] = nr[c] + fr[c];
+      nxC[c] = nr[D + c] + fr[D + c];
+    }
   }
-  // pre-sums of step n+1 = near + far
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    st.preP[c] = nr[c] + fr[c];
-    st.preC[c] = nr[D + c] + fr[D + c];
-    st.fc[c] = v[D + c];
+    st.preP[c] = nxP[c];
+    st.preC[c] = nxC[c];
   }
   return true;
 }
 
+// far handoffs of steps n+1 .. n+7 present?  (n % 8 == 0, n + 8 <= N: all
+// those steps are < N and lie in the 32-step chunk of n+1, whose handoff
+// happened ~25 steps ago.)  Plain loads issue in parallel; the fence then
+// orders the block's hbuf reads after them (fence-based acquire).
+__device__ __forceinline__ bool leader_block_ready(StepperSmem& S, int n) {
+  bool ok = true;
+#pragma unroll
+  for (int u = 1; u <= 7; ++u) {
+    const int m = n + u;
+    ok &= ld_volatile_smem(&S.hflag[m & (kHR - 1)]) == m;
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  __threadfence_block();
+  return ok;
+}
+
 template <int D>
 __device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
-                                                   long long n_next, int lane, unsigned long long& throttled) {
+                                                   long long n_next, int lane, unsigned long long& throttled,
+                                                   unsigned long long& lag_sum) {
   if (st.err_kind != KIND_NONE) {
     if (lane == 0)
       raise_abort(P, ERR_NONFINITE, st.err_kind, st.err_step, static_cast<double>(st.err_step + 1) * P.h);
@@ -323,7 +368,9 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
   }
   // ring back-pressure: the writer warp and every helper warp must have
   // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
-  if (n_next - slowest_consumer(S) > kRing - 24) {
+  const long long lag = n_next - slowest_consumer(S);
+  lag_sum += static_cast<unsigned long long>(lag);
+  if (lag > kRing - 24) {
     unsigned spins = 0;
     const unsigned long long w0 = global_ns();
     while (n_next - slowest_consumer(S) > kRing - 24) {
@@ -374,29 +421,57 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) 
   if (!leader_wait_handoff(P, S, 0, waited)) return;
   {
     double nr[2 * D], fr[2 * D];
-    leader_gather<D>(S, st, 0, lane, nr, fr);
+    leader_gather<D, true>(S, st, 0, lane, nr, fr, true);
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       st.preP[c] = nr[c] + fr[c];
       st.preC[c] = nr[D + c] + fr[D + c];
     }
   }
-  leader_push<D, true>(S, st, 0, lane, f0);
+  leader_push<D>(st, leader_push_weights<true>(S, st.cA, 0, lane), f0);
 #pragma unroll
   for (int c = 0; c < D; ++c) st.fc[c] = f0[c];
 
-  long long n = 0;
-  while (n + 8 <= N) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (!leader_step<SYS, D>(P, S, st, b0, a0, n + u, lane, waited)) return;
+  const uint32_t bars_u32 = smem_u32(&S.bars[0]);
+  const int N32 = static_cast<int>(N);
+  const bool solo = (P.debug & 1) != 0;  // dev: leader ignores handoffs and back-pressure (results invalid)
+  const long long c_loop = clock64();
+  unsigned long long fast_blocks = 0, lag_sum = 0;
+  int n = 0;
+  // step 0 has no corrector interior (a0 term excluded); blocks start at 8
+  if (!leader_step<SYS, D, false, true>(P, S, st, b0, 0.0, 0, lane, bars_u32, waited)) return;
+  for (n = 1; n < 8 && n < N32; ++n)
+    if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
+  if (!leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
+  while (n + 8 <= N32) {
+    if (solo || leader_block_ready(S, n)) {
+      ++fast_blocks;
+      // n % 8 == 0: a 32-step chunk boundary (m1 % 32 == 0) can only be the
+      // last step, whose gather (step n+8) is checked on its own
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 0, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 1, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 2, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 3, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 4, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 5, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 6, lane, bars_u32, waited)) return;
+      if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n + 7, lane, bars_u32, waited)) return;
+    } else {
+#pragma unroll 1
+      for (int u = 0; u < 8; ++u)
+        if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n + u, lane, bars_u32, waited)) return;
+    }
     n += 8;
-    if (!leader_check_block<D>(P, S, st, n, lane, throttled)) return;
+    if (!solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   }
-  for (; n < N; ++n)
-    if (!leader_step<SYS, D>(P, S, st, b0, a0, n, lane, waited)) return;
-  if (!leader_check_block<D>(P, S, st, n, lane, throttled)) return;
+#pragma unroll 1
+  for (; n < N32; ++n)
+    if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
+  if (!solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   if (lane == 0) {
+    P.ctrl->prof[0] = static_cast<unsigned long long>(clock64() - c_loop);
+    P.ctrl->prof[1] = fast_blocks;
+    P.ctrl->prof[2] = lag_sum;
     P.ctrl->leader_wait_ns = waited;
     P.ctrl->leader_throttle_ns = throttled;
   }
@@ -454,43 +529,37 @@ __device__ __forceinline__ bool helper_handoff(const EngineParams& P, StepperSme
   return true;
 }
 
-template <int D, bool FIRST>
-__device__ __forceinline__ bool helper_consume(const EngineParams& P, StepperSmem& S, int k, int N,
-                                               int (&m)[kSlotsPerThread], int (&lo)[kSlotsPerThread],
-                                               double (&accP)[kSlotsPerThread][D],
-                                               double (&accC)[kSlotsPerThread][D], double* f0) {
-  double fk[D];
-  const double* row = &S.ring[k % kRing][0];
+// Push the published f_k, k in [k0, k0 + 8) (those <= kl), into this
+// thread's far slots.  Batches are 8-aligned, and both ends of a slot's far
+// window -- lo(m) (a multiple of 128) and kh(m) = 32(c-1) - 1 (== 7 mod 8) --
+// are batch boundaries, so the window test is one predicate per slot per
+// batch and the unrolled body is branch-free.
+template <int D>
+__device__ __forceinline__ void helper_batch(const StepperSmem& S, int k0, int kl, const int (&m)[kSlotsPerThread],
+                                             const bool (&in)[kSlotsPerThread],
+                                             double (&accP)[kSlotsPerThread][D],
+                                             double (&accC)[kSlotsPerThread][D]) {
 #pragma unroll
-  for (int c = 0; c < D; ++c) fk[c] = row[D + c];
-  if (FIRST) {
+  for (int i = 0; i < kBatch; ++i) {
+    const int k = k0 + i;
+    const bool live = k <= kl;
+    double fk[D];
+    const double* row = &S.ring[k & (kRing - 1)][0];
 #pragma unroll
-    for (int c = 0; c < D; ++c) f0[c] = fk[c];
-  }
+    for (int c = 0; c < D; ++c) fk[c] = live ? row[D + c] : 0.0;  // entries past kl may be unwritten
 #pragma unroll
-  for (int s = 0; s < kSlotsPerThread; ++s) {
-    const int j = m[s] - k;
-    const int kh = (m[s] & ~(kChunk - 1)) - kChunk - 1;  // last far term: 32(c-1) - 1
-    const bool in = (k >= lo[s]) & (k <= kh);
-    const int jj = in ? j : 0;
-    const double wb = in ? S.wb[jj] : 0.0;
-    const double wa = (in && !FIRST) ? S.wa[jj] : 0.0;  // corrector interior excludes k = 0
+    for (int s = 0; s < kSlotsPerThread; ++s) {
+      const bool on = in[s] & live;
+      const int jj = on ? m[s] - k : 0;
+      const double wb = on ? S.wb[jj] : 0.0;
+      const double wa = on ? S.wa[jj] : 0.0;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      accP[s][c] = fma(wb, fk[c], accP[s][c]);
-      accC[s][c] = fma(wa, fk[c], accC[s][c]);
-    }
-    // slots of chunks 0 and 1 hand off after f_0; every other slot after f_kh
-    const bool due = FIRST ? (kh <= 0) : (k == kh);
-    if (due && m[s] < N) {
-      if (!helper_handoff<D>(P, S, m[s], f0, accP[s], accC[s])) return false;
-      m[s] += kSlots;
-      lo[s] = static_cast<int>(lo_of(m[s]));
-#pragma unroll
-      for (int c = 0; c < D; ++c) { accP[s][c] = 0.0; accC[s][c] = 0.0; }
+      for (int c = 0; c < D; ++c) {
+        accP[s][c] = fma(wb, fk[c], accP[s][c]);
+        accC[s][c] = fma(wa, fk[c], accC[s][c]);
+      }
     }
   }
-  return true;
 }
 
 template <int D>
@@ -507,18 +576,19 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
 #pragma unroll
     for (int c = 0; c < D; ++c) { accP[s][c] = 0.0; accC[s][c] = 0.0; }
   }
-#pragma unroll
-  for (int c = 0; c < D; ++c) f0[c] = 0.0;
+  long long c_wait = 0, c_proc = 0;  // dev statistics (helper warp 1)
 
-  // batches [0], [1, kBatch], [kBatch+1, 2 kBatch], ...: step 0 alone, since
-  // the handoffs of chunks 0 and 1 need only f_0 and the leader waits for them
-  for (int k0 = 0, kl = 0; k0 <= N; k0 = kl + 1, kl = (k0 + kBatch - 1 < N) ? k0 + kBatch - 1 : N) {
+  // batches [0], [1, 7], [8, 15], [16, 23], ...: step 0 alone, since the
+  // handoffs of chunks 0 and 1 need only f_0 and the leader waits for them
+  for (int k0 = 0, kl = 0; k0 <= N; k0 = kl + 1, kl = (((k0 | (kBatch - 1)) < N) ? (k0 | (kBatch - 1)) : N)) {
     uint64_t* bar = &S.bars[kl % kNumBars];
     const uint32_t par = static_cast<uint32_t>((kl / kNumBars) & 1);
+    const long long c_w = clock64();
     if (!mbar_test(bar, par)) {
       unsigned spins = 0;
       const unsigned long long w0 = global_ns();
-      while (!mbar_wait_hint(bar, par, 100000u)) {
+      const bool spin = (P.debug & 4) != 0;  // dev: poll without the suspend hint
+      while (!(spin ? mbar_test(bar, par) : mbar_wait_hint(bar, par, 100000u))) {
         if (ld_volatile_smem(&S.abort)) return;
         if (((++spins) & 255u) == 0) {
           if (*((volatile int*)&P.ctrl->abort)) return;
@@ -526,17 +596,53 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
         }
       }
     }
+    const long long c_p = clock64();
     if (k0 == 0) {
-      if (!helper_consume<D, true>(P, S, 0, N, m, lo, accP, accC, f0)) return;
-    } else {
+      // f_0: enters the predictor sums only (the corrector interior starts at
+      // k = 1; its k = 0 term is the first-node coefficient, added at handoff)
+      const double* row = &S.ring[0][0];
 #pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int k = k0 + i;
-        if (k <= kl && !helper_consume<D, false>(P, S, k, N, m, lo, accP, accC, f0)) return;
+      for (int c = 0; c < D; ++c) f0[c] = row[D + c];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int kh = (m[s] & ~(kChunk - 1)) - kChunk - 1;
+        const double wb = (lo[s] == 0 && kh >= 0) ? S.wb[m[s]] : 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) accP[s][c] = fma(wb, f0[c], accP[s][c]);
+      }
+    } else {
+      const bool skip = (P.debug & 2) != 0;  // dev: no far-window pushes (results invalid)
+      bool in[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const int kh = (m[s] & ~(kChunk - 1)) - kChunk - 1;  // last far term: 32(c-1) - 1
+        in[s] = (k0 >= lo[s]) & (kl <= kh) & !skip;
+      }
+      helper_batch<D>(S, k0, kl, m, in, accP, accC);
+    }
+    // handoffs: slots whose far window ends with this batch (chunks 0 and 1:
+    // with f_0).  One branch per slot per batch.
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int kh = (m[s] & ~(kChunk - 1)) - kChunk - 1;
+      const bool due = (k0 == 0) ? (kh <= 0) : (kl == kh);
+      if (due && m[s] < N) {
+        if (!helper_handoff<D>(P, S, m[s], f0, accP[s], accC[s])) return;
+        m[s] += kSlots;
+        lo[s] = static_cast<int>(lo_of(m[s]));
+#pragma unroll
+        for (int c = 0; c < D; ++c) { accP[s][c] = 0.0; accC[s][c] = 0.0; }
       }
     }
     __syncwarp();
     if (lane == 0) st_volatile_smem(&S.hprog[hwarp], kl);
+    const long long c_e = clock64();
+    c_wait += c_p - c_w;
+    c_proc += c_e - c_p;
+  }
+  if (hwarp == 1 && lane == 0) {
+    P.ctrl->prof[4] = static_cast<unsigned long long>(c_wait);
+    P.ctrl->prof[5] = static_cast<unsigned long long>(c_proc);
   }
 }
 
@@ -699,8 +805,10 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
   }
   __syncthreads();
   if (warp == 0) { stepper_leader<SYS, D>(P, S, lane); return; }
-  if (warp == 4) { stepper_writer<D>(P, S, lane); return; }
-  if (warp == 8) { stepper_publisher<D>(P, S, lane); return; }
+  // SMSP 0 (warps 0, 4, 8, 12) belongs to the leader alone: the writer and
+  // the publisher poll, and their issue slots would come out of the chain's
+  if (warp == kWriterWarp) { stepper_writer<D>(P, S, lane); return; }
+  if (warp == kPublisherWarp) { stepper_publisher<D>(P, S, lane); return; }
   if ((warp & 3) == 0) return;  // SMSP 0 stays with the leader warp
   const int hw = helper_index(warp);  // warps 1,2,3,5,6,7,9,10 -> 0..7
   if (hw >= kHelperWarps) return;
