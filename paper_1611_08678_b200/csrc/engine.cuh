@@ -818,6 +818,10 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
 // ======================================================================
 // BULK AGENTS
 // ======================================================================
+}  // namespace fabm
+#include "bulk_dmma.cuh"
+namespace fabm {
+
 struct AgentSmem {
   double w[2][4][kWCols];  // b, a in mod-4 transposed layout
   double f[kB][4];         // f tile of the source block (row stride 4)
@@ -922,7 +926,13 @@ __device__ __forceinline__ int owned_count(int agent, int nA, int n_targets) {
 }
 
 template <int D>
-__device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int lane, const ShardView& sv) {
+struct BulkSmem {
+  DmmaSmem<D> t;
+  int own_next[kMaxOwn];   // next source block per owned target
+};
+
+template <int D>
+__device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
   if (agent >= n_targets) return;
@@ -931,11 +941,8 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
   if (nown == 0) return;
   for (int i = lane; i < nown; i += 32) A.own_next[i] = 0;
   __syncwarp();
-  double accP[kR][D], accC[kR][D];
-#pragma unroll
-  for (int r = 0; r < kR; ++r)
-#pragma unroll
-    for (int c = 0; c < D; ++c) { accP[r][c] = 0.0; accC[r][c] = 0.0; }
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
   int cur = -1, done = 0;
   unsigned long long tiles = 0;
   unsigned long long last_progress = global_ns();
@@ -987,14 +994,11 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     last_progress = global_ns();
     const int J = owned_target(agent, best, nA);
     if (cur != best) {
-      if (cur >= 0) agent_store_acc<D>(sv.BK, owned_target(agent, cur, nA), lane, accP, accC);
+      if (cur >= 0) dmma_spill<D>(sv.BK, owned_target(agent, cur, nA), lane, acc);
       if (A.own_next[best] > 0) {
-        agent_load_acc<D>(sv.BK, J, lane, accP, accC);
+        dmma_reload<D>(sv.BK, J, lane, acc);
       } else {
-#pragma unroll
-        for (int r = 0; r < kR; ++r)
-#pragma unroll
-          for (int c = 0; c < D; ++c) { accP[r][c] = 0.0; accC[r][c] = 0.0; }
+        dmma_zero<D>(acc);
       }
       cur = best;
     }
@@ -1004,7 +1008,7 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     while (nx < lim) {
       int M2 = 0;
       if (lane == 0) M2 = P.n_shards == 1 ? ld_relaxed_gpu(&sv.ctrl->src_done) : ld_relaxed_sys(&sv.ctrl->src_done);
-      agent_tile<D>(P.wb, P.wa, sv.F, A, nx, J, lane, accP, accC);
+      dmma_chunk<D>(P.wb, P.wa, sv.F, A.t, J * kB, nx * kB, (J - kL + 1) * kB, lane, acc);
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
@@ -1015,7 +1019,8 @@ __device__ void bulk_agent(const EngineParams& P, AgentSmem& A, int agent, int l
     if (lane == 0) A.own_next[best] = nx;
     __syncwarp();
     if (nx == J - kL + 1) {
-      agent_store_acc<D>(P.BK, J, lane, accP, accC);  // shard 0's BK (peer memory on other GPUs)
+      __syncwarp();  // every lane's reload of this target's spill precedes the row-layout stores
+      dmma_store_rows<D>(P.BK, J, lane, acc);  // shard 0's BK (peer memory on other GPUs)
       if (P.n_shards == 1) {
         __threadfence();
         __syncwarp();
@@ -1050,7 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P)
     if (P.my_shard <= 0) stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
   } else {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    AgentSmem* A = reinterpret_cast<AgentSmem*>(smem_raw) + warp;
+    BulkSmem<D>* A = reinterpret_cast<BulkSmem<D>*>(smem_raw) + warp;
     const int lcta = blockIdx.x - 1;
     const int sh = P.my_shard >= 0 ? P.my_shard : lcta % P.n_shards;
     // agents are dealt warp-major across CTAs (of all shards) so every SM
@@ -1061,8 +1066,9 @@ __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P)
   }
 }
 
+template <int D>
 constexpr size_t engine_smem_bytes() {
-  return sizeof(StepperSmem) > kWarps * sizeof(AgentSmem) ? sizeof(StepperSmem) : kWarps * sizeof(AgentSmem);
+  return sizeof(StepperSmem) > kWarps * sizeof(BulkSmem<D>) ? sizeof(StepperSmem) : kWarps * sizeof(BulkSmem<D>);
 }
 
 }  // namespace fabm

@@ -95,7 +95,7 @@ using EngineLaunch = cudaError_t (*)(const EngineParams&, int grid, cudaStream_t
 template <int SYS, int D>
 cudaError_t launch_engine(const EngineParams& P, int grid, cudaStream_t stream) {
   auto kern = abm_engine_kernel<SYS, D>;
-  const size_t smem = engine_smem_bytes();
+  const size_t smem = engine_smem_bytes<D>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   EngineParams Pc = P;
@@ -106,7 +106,7 @@ cudaError_t launch_engine(const EngineParams& P, int grid, cudaStream_t stream) 
 template <int SYS, int D>
 cudaError_t engine_occupancy(int* blocks_per_sm) {
   auto kern = abm_engine_kernel<SYS, D>;
-  const size_t smem = engine_smem_bytes();
+  const size_t smem = engine_smem_bytes<D>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, kThreads, smem);
