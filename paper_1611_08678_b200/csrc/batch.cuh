@@ -8,9 +8,10 @@
 // ticket counter in the order u -> (t = u mod T, J = u div T), so all
 // trajectories advance together and the last wave is evenly filled.  A unit:
 //   1. pulls the bulk of its 128 targets from every completed block I < J:
-//      J Toeplitz tiles (the same register-blocked tile as the single-
-//      trajectory agents) in ascending I — a fixed FMA order, independent of
-//      which warp runs the unit, so results are bitwise deterministic;
+//      J Toeplitz chunks on the FP64 tensor cores (bulk_dmma.cuh, the same
+//      sweep as the single-trajectory agents) in ascending I — a fixed order,
+//      independent of which warp runs the unit, so results are bitwise
+//      deterministic;
 //   2. steps through the block: all 32 lanes run the sequential chain
 //      (serial.py:150-170) redundantly; lane l holds the sums of steps
 //      JB+4l..JB+4l+3 and pushes every new f_k into them (in-block window).
@@ -45,7 +46,7 @@ struct BatchParams {
 };
 
 template <int SYS, int D>
-__device__ void batch_unit(const BatchParams& P, AgentSmem& A, int t, int J, int lane) {
+__device__ void batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int lane) {
   constexpr int DS = Stride<D>::value;
   const long long N = P.N;
   const double* wb = P.W + static_cast<long long>(t) * 3 * P.WL;
@@ -64,14 +65,36 @@ __device__ void batch_unit(const BatchParams& P, AgentSmem& A, int t, int J, int
   const double ha = P.ha[t], ig = P.ig[t];
   const long long JB = static_cast<long long>(J) * kB;
 
-  // ---- 1. bulk of sources I < J (ascending), in registers
+  // ---- 1. bulk of sources I < J (ascending), then re-dealt through shared
+  // memory from the DMMA layout to the stepping layout (lane l: steps 4l..4l+3)
   double accP[kR][D], accC[kR][D];
+  {
+    DmmaAcc<D> acc;
+    dmma_zero<D>(acc);
+    for (int I = 0; I < J; ++I) dmma_chunk<D>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
+    __syncwarp();
+    double* rows = &A.f[0][0];  // [B][2][D]
 #pragma unroll
-  for (int r = 0; r < kR; ++r)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int c = 0; c < D; ++c) { accP[r][c] = 0.0; accC[r][c] = 0.0; }
-  for (int I = 0; I < J; ++I) agent_tile<D>(wb, wa, F, A, I, J, lane, accP, accC);
-  __syncwarp();
+      for (int e = 0; e < 2; ++e) {
+        const int tt = dmma_target(lane, h, e);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          rows[(tt * 2 + 0) * D + c] = acc[h][c][0][e];
+          rows[(tt * 2 + 1) * D + c] = acc[h][c][1][e];
+        }
+      }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        accP[r][c] = rows[((kR * lane + r) * 2 + 0) * D + c];
+        accC[r][c] = rows[((kR * lane + r) * 2 + 1) * D + c];
+      }
+    __syncwarp();
+  }
 
   // ---- 2. state at the block start: f_JB (and f_0), first-node terms
   double f0[D], fc[D];
@@ -95,9 +118,9 @@ __device__ void batch_unit(const BatchParams& P, AgentSmem& A, int t, int J, int
 #pragma unroll
     for (int c = 0; c < D; ++c) { f0[c] = __ldcg(F + c); fc[c] = __ldcg(F + JB * DS + c); }
   }
-  // in-block weights: tb[j + 128] = b_j for 1 <= j < B, 0 otherwise (A.f is free now)
-  double* tb = &A.f[0][0];
-  double* ta = tb + 2 * kB;
+  // in-block weights: tb[j + 128] = b_j for 1 <= j < B, 0 otherwise (A.w is free now)
+  double* tb = &A.w[0][0];
+  double* ta = &A.w[1][0];
   for (int i = lane; i < 2 * kB; i += 32) {
     const int j = i - kB;
     tb[i] = (j >= 1) ? __ldg(wb + j) : 0.0;
@@ -198,7 +221,7 @@ template <int SYS, int D>
 __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  AgentSmem& A = reinterpret_cast<AgentSmem*>(smem_raw)[warp];
+  DmmaSmem<D>& A = reinterpret_cast<DmmaSmem<D>*>(smem_raw)[warp];
   const unsigned long long total = static_cast<unsigned long long>(P.T) * P.nb;
   for (;;) {
     unsigned long long u = 0;

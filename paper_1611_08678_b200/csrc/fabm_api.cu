@@ -685,7 +685,7 @@ using BatchLaunch = cudaError_t (*)(const BatchParams&, int grid, cudaStream_t);
 template <int SYS, int D>
 cudaError_t launch_batch(const BatchParams& P, int grid, cudaStream_t stream) {
   auto kern = abm_batch_kernel<SYS, D>;
-  const size_t smem = kWarps * sizeof(AgentSmem);
+  const size_t smem = kWarps * sizeof(DmmaSmem<D>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, stream>>>(P);
