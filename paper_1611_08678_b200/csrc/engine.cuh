@@ -641,8 +641,8 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
     c_proc += c_e - c_p;
   }
   if (hwarp == 1 && lane == 0) {
-    P.ctrl->prof[4] = static_cast<unsigned long long>(c_wait);
-    P.ctrl->prof[5] = static_cast<unsigned long long>(c_proc);
+    P.ctrl->prof[3] = static_cast<unsigned long long>(c_wait);
+    P.ctrl->prof[7] = static_cast<unsigned long long>(c_proc);
   }
 }
 
