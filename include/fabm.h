@@ -45,7 +45,8 @@ enum {
   FABM_ERR_CONFIG = 2,    /* ValueError: bad alpha/dim/y0/grid/system */
   FABM_ERR_TIMEOUT = 3,   /* StrategyTimeoutError: device watchdog expired */
   FABM_ERR_CUDA = 4,      /* CUDA runtime failure (message in status) */
-  FABM_ERR_NODEVICE = 5   /* no usable sm_100 device */
+  FABM_ERR_NODEVICE = 5,  /* no usable sm_100 device */
+  FABM_ERR_IO = 6         /* OSError: the output file could not be written */
 };
 
 /* which rhs evaluation failed (fabm_status.kind) */
@@ -201,6 +202,31 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids,
                      int64_t count, int device, double* states,
                      double* f_cache, double* y_last, double* kernel_ms,
                      fabm_status* status);
+
+/* ---- trajectory CSV output: replaces write_trajectory_csv (cli.py:97-105) --
+ * Bytes identical to the reference's Python loop: header "t,y0,..,y{d-1}\n",
+ * then one row per time point, every value as CPython's f"{v:.17g}"
+ * (correctly rounded, ties to even, trailing zeros removed).  The values are
+ * formatted on the GPU (csrc/csv_format.cuh).
+ *   states : host, n_rows * dim doubles (Trajectory.states, row-major)
+ *   t      : host, n_rows doubles (Trajectory.t), or NULL for t[n] = n * h
+ *            (GridSpec.times(), core.py:179-181)
+ *   kernel_ms (optional out): device time of the formatting kernels
+ * fabm_format_csv writes into a caller buffer: if out_cap is too small it
+ * returns FABM_ERR_CONFIG with *n_bytes = the size needed (out may be NULL).
+ * fabm_write_csv creates/truncates `path` like open(path, "w") and returns
+ * FABM_ERR_IO if it cannot be written. */
+int fabm_format_csv(const double* states, const double* t, int64_t n_rows,
+                    int32_t dim, double h, int device, char* out,
+                    int64_t out_cap, int64_t* n_bytes, double* kernel_ms,
+                    fabm_status* status);
+int fabm_write_csv(const char* path, const double* states, const double* t,
+                   int64_t n_rows, int32_t dim, double h, int device,
+                   int64_t* n_bytes, double* kernel_ms, fabm_status* status);
+/* the CSV of the plan's last run straight from its device-resident states
+ * (no D2H of the trajectory; t[n] = n * h) */
+int fabm_plan_write_csv(fabm_plan* plan, const char* path, int64_t* n_bytes,
+                        double* kernel_ms, fabm_status* status);
 
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
 /* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */

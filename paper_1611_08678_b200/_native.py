@@ -25,6 +25,7 @@ FABM_ERR_CONFIG = 2
 FABM_ERR_TIMEOUT = 3
 FABM_ERR_CUDA = 4
 FABM_ERR_NODEVICE = 5
+FABM_ERR_IO = 6
 
 WEIGHTS_ACCURATE = 0
 WEIGHTS_FORMULA = 1
@@ -56,6 +57,9 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_detach_shards",
     "fabm_solve_batch",
     "fabm_measure_dfma_peak",
+    "fabm_format_csv",
+    "fabm_write_csv",
+    "fabm_plan_write_csv",
 )
 
 
@@ -111,6 +115,7 @@ class Stats(ctypes.Structure):
 
 
 _DP = ctypes.POINTER(ctypes.c_double)
+_I64P = ctypes.POINTER(ctypes.c_int64)
 _lib = None
 
 
@@ -138,6 +143,11 @@ def _declare(lib):
         "fabm_plan_detach_shards": (ctypes.c_int, [plan, S]),
         "fabm_solve_batch": (ctypes.c_int, [P, G, ctypes.c_int64, ctypes.c_int, _DP, _DP, _DP, _DP, S]),
         "fabm_measure_dfma_peak": (ctypes.c_double, [ctypes.c_int]),
+        "fabm_format_csv": (ctypes.c_int, [_DP, _DP, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int,
+                                           ctypes.c_char_p, ctypes.c_int64, _I64P, _DP, S]),
+        "fabm_write_csv": (ctypes.c_int, [ctypes.c_char_p, _DP, _DP, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
+                                          ctypes.c_int, _I64P, _DP, S]),
+        "fabm_plan_write_csv": (ctypes.c_int, [plan, ctypes.c_char_p, _I64P, _DP, S]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

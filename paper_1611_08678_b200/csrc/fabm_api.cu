@@ -11,10 +11,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cerrno>
+#include <string>
 #include <vector>
 
 #include "../../include/fabm.h"
 #include "batch.cuh"
+#include "csv_format.cuh"
 #include "engine.cuh"
 #include "weights.cuh"
 
@@ -941,6 +944,241 @@ double fabm_measure_dfma_peak(int device) {
   cudaFree(out);
   const double fmas = static_cast<double>(blocks) * threads * iters * 8.0;
   return fmas / (best * 1e-3);
+}
+
+}  // extern "C"
+
+// ======================================================================
+// Trajectory CSV (cli.py:97-105) — formatting kernels in csv_format.cuh
+// ======================================================================
+namespace {
+
+std::string csv_header(int dim) {
+  std::string h = "t";
+  for (int i = 0; i < dim; ++i) h += ",y" + std::to_string(i);
+  h += "\n";
+  return h;
+}
+
+// The CSV of device states (and optional device times) into a fresh device
+// buffer *d_out of *n_bytes (header included).  Synchronous on `stream`.
+int csv_format_device(const double* d_states, const double* d_t, double h, long long n_rows, int dim,
+                      cudaStream_t stream, char** d_out, long long* n_bytes, double* kernel_ms,
+                      fabm_status* status) {
+  *d_out = nullptr;
+  *n_bytes = 0;
+  const int rows = fabm_csv::tile_rows(dim);
+  if (dim < 1 || rows < 32 || n_rows < 0) {
+    set_status(status, FABM_ERR_CONFIG, "csv: need dim >= 1 (at most %d) and n_rows >= 0", 280);
+    return FABM_ERR_CONFIG;
+  }
+  const std::string head = csv_header(dim);
+  const long long n_tiles = (n_rows + rows - 1) / rows;
+  int* row_len = nullptr;
+  long long* tile_off = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  auto cleanup = [&]() {
+    if (row_len) cudaFree(row_len);
+    if (tile_off) cudaFree(tile_off);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+  };
+#define CSV_TRY(expr)                                                               \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      set_status(status, FABM_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e));   \
+      cleanup();                                                                    \
+      if (*d_out) { cudaFree(*d_out); *d_out = nullptr; }                           \
+      return FABM_ERR_CUDA;                                                         \
+    }                                                                               \
+  } while (0)
+  CSV_TRY(cudaEventCreate(&e0));
+  CSV_TRY(cudaEventCreate(&e1));
+  CSV_TRY(cudaMalloc(&row_len, sizeof(int) * (n_rows > 0 ? n_rows : 1)));
+  CSV_TRY(cudaMalloc(&tile_off, sizeof(long long) * (n_tiles + 1)));
+  CSV_TRY(cudaMemsetAsync(tile_off, 0, sizeof(long long) * (n_tiles + 1), stream));
+  float ms_a = 0.f, ms_b = 0.f;
+  long long body = 0;
+  if (n_tiles > 0) {
+    CSV_TRY(cudaEventRecord(e0, stream));
+    fabm_csv::csv_len_kernel<<<static_cast<unsigned>(n_tiles), rows, 0, stream>>>(d_states, d_t, h, n_rows, dim,
+                                                                                   row_len, tile_off);
+    CSV_TRY(cudaGetLastError());
+    fabm_csv::csv_scan_kernel<<<1, 1024, 0, stream>>>(tile_off, n_tiles);
+    CSV_TRY(cudaGetLastError());
+    CSV_TRY(cudaEventRecord(e1, stream));
+    CSV_TRY(cudaMemcpyAsync(&body, tile_off + n_tiles, sizeof(long long), cudaMemcpyDeviceToHost, stream));
+    CSV_TRY(cudaStreamSynchronize(stream));
+    CSV_TRY(cudaEventElapsedTime(&ms_a, e0, e1));
+  }
+  const long long total = static_cast<long long>(head.size()) + body;
+  CSV_TRY(cudaMalloc(d_out, total > 0 ? total : 1));
+  CSV_TRY(cudaMemcpyAsync(*d_out, head.data(), head.size(), cudaMemcpyHostToDevice, stream));
+  if (n_tiles > 0) {
+    const size_t smem = fabm_csv::tile_smem_bytes(dim, rows);
+    CSV_TRY(cudaFuncSetAttribute(fabm_csv::csv_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    CSV_TRY(cudaEventRecord(e0, stream));
+    fabm_csv::csv_write_kernel<<<static_cast<unsigned>(n_tiles), rows, smem, stream>>>(
+        d_states, d_t, h, n_rows, dim, row_len, tile_off, *d_out + head.size());
+    CSV_TRY(cudaGetLastError());
+    CSV_TRY(cudaEventRecord(e1, stream));
+  }
+  CSV_TRY(cudaStreamSynchronize(stream));
+  if (n_tiles > 0) CSV_TRY(cudaEventElapsedTime(&ms_b, e0, e1));
+#undef CSV_TRY
+  cleanup();
+  *n_bytes = total;
+  if (kernel_ms) *kernel_ms = static_cast<double>(ms_a) + ms_b;
+  return FABM_OK;
+}
+
+// Device bytes -> file, through two pinned staging buffers so the D2H of
+// chunk i+1 overlaps the write of chunk i.
+int csv_write_file(const char* path, const char* d_bytes, long long n, cudaStream_t stream, fabm_status* status) {
+  if (!path) { set_status(status, FABM_ERR_CONFIG, "csv: null path"); return FABM_ERR_CONFIG; }
+  FILE* fh = std::fopen(path, "wb");
+  if (!fh) {
+    set_status(status, FABM_ERR_IO, "%s: %s", path, std::strerror(errno));
+    return FABM_ERR_IO;
+  }
+  constexpr long long kChunk = 32ll << 20;
+  char* pin[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int rc = FABM_OK;
+  auto fail_cuda = [&](const char* what, cudaError_t e) {
+    set_status(status, FABM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    rc = FABM_ERR_CUDA;
+  };
+  cudaError_t e;
+  for (int i = 0; i < 2 && rc == FABM_OK; ++i) {
+    if ((e = cudaMallocHost(&pin[i], kChunk)) != cudaSuccess) fail_cuda("cudaMallocHost", e);
+    else if ((e = cudaEventCreate(&done[i])) != cudaSuccess) fail_cuda("cudaEventCreate", e);
+  }
+  const long long n_chunks = (n + kChunk - 1) / kChunk;
+  auto issue = [&](long long c) {
+    const long long off = c * kChunk, len = std::min(kChunk, n - off);
+    cudaError_t ee = cudaMemcpyAsync(pin[c & 1], d_bytes + off, len, cudaMemcpyDeviceToHost, stream);
+    if (ee == cudaSuccess) ee = cudaEventRecord(done[c & 1], stream);
+    if (ee != cudaSuccess) fail_cuda("csv D2H", ee);
+  };
+  if (rc == FABM_OK && n_chunks > 0) issue(0);
+  for (long long c = 0; c < n_chunks && rc == FABM_OK; ++c) {
+    if ((e = cudaEventSynchronize(done[c & 1])) != cudaSuccess) { fail_cuda("csv D2H sync", e); break; }
+    if (c + 1 < n_chunks) issue(c + 1);
+    const long long len = std::min(kChunk, n - c * kChunk);
+    if (std::fwrite(pin[c & 1], 1, static_cast<size_t>(len), fh) != static_cast<size_t>(len)) {
+      set_status(status, FABM_ERR_IO, "%s: %s", path, std::strerror(errno));
+      rc = FABM_ERR_IO;
+    }
+  }
+  cudaStreamSynchronize(stream);
+  if (std::fclose(fh) != 0 && rc == FABM_OK) {
+    set_status(status, FABM_ERR_IO, "%s: %s", path, std::strerror(errno));
+    rc = FABM_ERR_IO;
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (pin[i]) cudaFreeHost(pin[i]);
+    if (done[i]) cudaEventDestroy(done[i]);
+  }
+  return rc;
+}
+
+// host states/t -> device (one stream), for the host-pointer entry points
+int csv_upload(const double* states, const double* t, long long n_rows, int dim, int device, cudaStream_t* stream,
+               double** d_states, double** d_t, fabm_status* status) {
+  *d_states = nullptr;
+  *d_t = nullptr;
+  if (n_rows < 0 || dim < 1 || (n_rows > 0 && !states)) {
+    set_status(status, FABM_ERR_CONFIG, "csv: need states for n_rows >= 0 rows of dim >= 1");
+    return FABM_ERR_CONFIG;
+  }
+  const int ndev = fabm_device_count();
+  if (ndev <= 0 || device < 0 || device >= ndev) {
+    set_status(status, FABM_ERR_NODEVICE, "no CUDA device %d (found %d)", device, ndev);
+    return FABM_ERR_NODEVICE;
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaStreamCreateWithFlags(stream, cudaStreamNonBlocking));
+  const size_t sb = sizeof(double) * static_cast<size_t>(n_rows > 0 ? n_rows : 1) * dim;
+  CUDA_TRY(cudaMalloc(d_states, sb));
+  if (n_rows > 0)
+    CUDA_TRY(cudaMemcpyAsync(*d_states, states, sizeof(double) * n_rows * dim, cudaMemcpyHostToDevice, *stream));
+  if (t && n_rows > 0) {
+    CUDA_TRY(cudaMalloc(d_t, sizeof(double) * n_rows));
+    CUDA_TRY(cudaMemcpyAsync(*d_t, t, sizeof(double) * n_rows, cudaMemcpyHostToDevice, *stream));
+  }
+  return FABM_OK;
+}
+
+void csv_release(cudaStream_t stream, double* d_states, double* d_t, char* d_out) {
+  if (stream) cudaStreamSynchronize(stream);
+  if (d_states) cudaFree(d_states);
+  if (d_t) cudaFree(d_t);
+  if (d_out) cudaFree(d_out);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fabm_format_csv(const double* states, const double* t, int64_t n_rows, int32_t dim, double h, int device,
+                    char* out, int64_t out_cap, int64_t* n_bytes, double* kernel_ms, fabm_status* status) {
+  clear_status(status);
+  cudaStream_t stream = nullptr;
+  double *d_states = nullptr, *d_t = nullptr;
+  char* d_out = nullptr;
+  int rc = csv_upload(states, t, n_rows, dim, device, &stream, &d_states, &d_t, status);
+  long long total = 0;
+  if (rc == FABM_OK) rc = csv_format_device(d_states, d_t, h, n_rows, dim, stream, &d_out, &total, kernel_ms, status);
+  if (rc == FABM_OK) {
+    if (n_bytes) *n_bytes = total;
+    if (!out || out_cap < total) {
+      set_status(status, FABM_ERR_CONFIG, "csv: output buffer of %lld bytes, %lld needed",
+                 static_cast<long long>(out_cap), total);
+      rc = FABM_ERR_CONFIG;
+    } else {
+      cudaError_t e = cudaMemcpyAsync(out, d_out, total, cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) {
+        set_status(status, FABM_ERR_CUDA, "csv D2H: %s", cudaGetErrorString(e));
+        rc = FABM_ERR_CUDA;
+      }
+    }
+  }
+  csv_release(stream, d_states, d_t, d_out);
+  return rc;
+}
+
+int fabm_write_csv(const char* path, const double* states, const double* t, int64_t n_rows, int32_t dim, double h,
+                   int device, int64_t* n_bytes, double* kernel_ms, fabm_status* status) {
+  clear_status(status);
+  cudaStream_t stream = nullptr;
+  double *d_states = nullptr, *d_t = nullptr;
+  char* d_out = nullptr;
+  int rc = csv_upload(states, t, n_rows, dim, device, &stream, &d_states, &d_t, status);
+  long long total = 0;
+  if (rc == FABM_OK) rc = csv_format_device(d_states, d_t, h, n_rows, dim, stream, &d_out, &total, kernel_ms, status);
+  if (rc == FABM_OK) rc = csv_write_file(path, d_out, total, stream, status);
+  if (rc == FABM_OK && n_bytes) *n_bytes = total;
+  csv_release(stream, d_states, d_t, d_out);
+  return rc;
+}
+
+int fabm_plan_write_csv(fabm_plan* p, const char* path, int64_t* n_bytes, double* kernel_ms, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  char* d_out = nullptr;
+  long long total = 0;
+  int rc = csv_format_device(p->Y, nullptr, p->grid.h, p->N + 1, p->prob.dim, p->stream, &d_out, &total, kernel_ms,
+                             status);
+  if (rc == FABM_OK) rc = csv_write_file(path, d_out, total, p->stream, status);
+  if (rc == FABM_OK && n_bytes) *n_bytes = total;
+  if (d_out) cudaFree(d_out);
+  return rc;
 }
 
 }  // extern "C"

@@ -206,6 +206,12 @@ class GpuPlan:
             _raise_status(st)
         return out
 
+    def write_csv(self, path, *, stats: dict | None = None) -> None:
+        """The last run's trajectory as the reference CSV (cli.py:97-105), formatted on the device."""
+        from .output import plan_write_csv
+
+        plan_write_csv(self, path, stats=stats)
+
     def stats(self) -> dict:
         s = nat.Stats()
         self._lib.fabm_plan_stats(self._h, ctypes_ref(s))

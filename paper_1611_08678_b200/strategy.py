@@ -9,6 +9,10 @@ drives the B200 engine under the name ``"gpu"``:
   block and reduction, with their bitwise repeat check (bench.py:80-87)
 * ``fodeabm.cli.solve_with_strategy`` does the same (cli.py:86-94) and the
   ``--strategy`` flag accepts ``gpu`` (cli.py:171)
+* ``fodeabm.cli.write_trajectory_csv`` (cli.py:97-105) is replaced by the
+  device formatter (:func:`paper_1611_08678_b200.output.write_trajectory_csv`,
+  byte-identical output), so ``fodeabm run`` writes its CSV from the GPU for
+  every strategy
 
 Problems built with the reference's own rhs factories run unchanged (see
 :func:`paper_1611_08678_b200.systems.adopt_reference_rhs`).  ``uninstall()``
@@ -19,6 +23,7 @@ from __future__ import annotations
 
 import importlib
 
+from .output import write_trajectory_csv
 from .solver import STRATEGY_NAME, solve_gpu
 
 __all__ = ["install", "uninstall"]
@@ -37,6 +42,7 @@ def install(weights: str = "accurate"):
     _SAVED["_solve_once"] = bench._solve_once
     _SAVED["solve_with_strategy"] = cli.solve_with_strategy
     _SAVED["_build_parser"] = cli._build_parser
+    _SAVED["write_trajectory_csv"] = cli.write_trajectory_csv
     orig_once = bench._solve_once
     orig_solve = cli.solve_with_strategy
     orig_parser = cli._build_parser
@@ -62,6 +68,7 @@ def install(weights: str = "accurate"):
     bench._solve_once = _solve_once
     cli.solve_with_strategy = solve_with_strategy
     cli._build_parser = _build_parser
+    cli.write_trajectory_csv = write_trajectory_csv
     return fodeabm
 
 
@@ -74,6 +81,7 @@ def uninstall():
     bench._solve_once = _SAVED["_solve_once"]
     cli.solve_with_strategy = _SAVED["solve_with_strategy"]
     cli._build_parser = _SAVED["_build_parser"]
+    cli.write_trajectory_csv = _SAVED["write_trajectory_csv"]
     _SAVED.clear()
 
 

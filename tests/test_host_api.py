@@ -226,6 +226,10 @@ class TestStrategyPlugin:
         args = cli._build_parser().parse_args(["solve", "--system", "linear", "--alpha", "0.5", "--tmax", "1",
                                                "--steps", "16", "--strategy", "gpu"])
         assert args.strategy == "gpu"
+        # the CSV writer is the device formatter while installed (byte-identical, §8f row 2)
+        from paper_1611_08678_b200.output import write_trajectory_csv as device_writer
+
+        assert cli.write_trajectory_csv is device_writer
         # other strategies still reach the reference implementations
         traj = bench._solve_once(problem, "serial", 16, 1, 1024)
         assert traj.states.shape == (17, 1)

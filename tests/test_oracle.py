@@ -119,3 +119,22 @@ def test_c1_against_mittag_leffler():
     err = np.abs(g["states"][::50, 0] - exact)
     assert err.max() <= 4e-5
     assert abs(g["states"][-1, 0] - 0.042979301317701527263) <= 1e-6
+
+
+# ---- trajectory CSV (cli.py:97-105): the oracle pinned to the reference's own files
+def _csv_case(name):
+    import gzip
+
+    from conftest import GOLDEN
+
+    with np.load(GOLDEN / "csv_inputs.npz") as z:
+        states, t = z[f"{name}_states"], z[f"{name}_t"]
+    return states, t, gzip.decompress((GOLDEN / f"csv_{name}.csv.gz").read_bytes())
+
+
+@pytest.mark.parametrize("name", ["c1_linear", "hr", "values"])
+def test_csv_oracle_matches_reference_files(name):
+    from oracle import csv_oracle
+
+    states, t, ref = _csv_case(name)
+    assert csv_oracle.format_csv(states, t) == ref
