@@ -228,6 +228,17 @@ int fabm_write_csv(const char* path, const double* states, const double* t,
 int fabm_plan_write_csv(fabm_plan* plan, const char* path, int64_t* n_bytes,
                         double* kernel_ms, fabm_status* status);
 
+/* ---- analytic oracle on the device: replaces mittag_leffler (verify.py:28-64)
+ * E_alpha(z) for n pairs (host arrays alpha[n], z[n] -> out[n]), the
+ * reference's log-space power series with Kahan summation, one thread per
+ * pair.  codes[n] (optional): 0 ok; 1 invalid argument (the reference's
+ * ValueError: alpha outside (0, 1], |z| > 10 or z not finite; out = nan);
+ * 2 a term overflowed (out = +-inf, as the reference returns); 3 no
+ * convergence in 20000 terms (the reference's ArithmeticError). */
+int fabm_mittag_leffler(const double* alpha, const double* z, int64_t n,
+                        int device, double* out, int32_t* codes,
+                        fabm_status* status);
+
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
 /* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */
 double fabm_measure_dfma_peak(int device);

@@ -60,6 +60,7 @@ EXPORTED_SYMBOLS = (
     "fabm_format_csv",
     "fabm_write_csv",
     "fabm_plan_write_csv",
+    "fabm_mittag_leffler",
 )
 
 
@@ -148,6 +149,8 @@ def _declare(lib):
         "fabm_write_csv": (ctypes.c_int, [ctypes.c_char_p, _DP, _DP, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
                                           ctypes.c_int, _I64P, _DP, S]),
         "fabm_plan_write_csv": (ctypes.c_int, [plan, ctypes.c_char_p, _I64P, _DP, S]),
+        "fabm_mittag_leffler": (ctypes.c_int, [_DP, _DP, ctypes.c_int64, ctypes.c_int, _DP,
+                                               ctypes.POINTER(ctypes.c_int32), S]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -18,6 +18,7 @@
 #include "../../include/fabm.h"
 #include "batch.cuh"
 #include "csv_format.cuh"
+#include "oracles.cuh"
 #include "engine.cuh"
 #include "weights.cuh"
 
@@ -1182,3 +1183,41 @@ int fabm_plan_write_csv(fabm_plan* p, const char* path, int64_t* n_bytes, double
 }
 
 }  // extern "C"
+
+extern "C" int fabm_mittag_leffler(const double* alpha, const double* z, int64_t n, int device, double* out,
+                                   int32_t* codes, fabm_status* status) {
+  clear_status(status);
+  if (n < 0 || (n > 0 && (!alpha || !z || !out))) {
+    set_status(status, FABM_ERR_CONFIG, "mittag_leffler: need alpha, z and out for n >= 0 pairs");
+    return FABM_ERR_CONFIG;
+  }
+  if (n == 0) return FABM_OK;
+  const int ndev = fabm_device_count();
+  if (ndev <= 0 || device < 0 || device >= ndev) {
+    set_status(status, FABM_ERR_NODEVICE, "no CUDA device %d (found %d)", device, ndev);
+    return FABM_ERR_NODEVICE;
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  double* d = nullptr;
+  int* c = nullptr;
+  const size_t nb = sizeof(double) * static_cast<size_t>(n);
+  cudaError_t e = cudaMalloc(&d, 3 * nb);
+  if (e == cudaSuccess) e = cudaMalloc(&c, sizeof(int) * static_cast<size_t>(n));
+  if (e == cudaSuccess) e = cudaMemcpy(d, alpha, nb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, z, nb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    const int threads = 128;
+    fabm_oracle::mittag_leffler_kernel<<<static_cast<unsigned>((n + threads - 1) / threads), threads>>>(
+        d, d + n, n, d + 2 * n, c);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out, d + 2 * n, nb, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && codes) e = cudaMemcpy(codes, c, sizeof(int) * static_cast<size_t>(n), cudaMemcpyDeviceToHost);
+  if (d) cudaFree(d);
+  if (c) cudaFree(c);
+  if (e != cudaSuccess) {
+    set_status(status, FABM_ERR_CUDA, "mittag_leffler: %s", cudaGetErrorString(e));
+    return FABM_ERR_CUDA;
+  }
+  return FABM_OK;
+}

@@ -13,6 +13,9 @@ drives the B200 engine under the name ``"gpu"``:
   device formatter (:func:`paper_1611_08678_b200.output.write_trajectory_csv`,
   byte-identical output), so ``fodeabm run`` writes its CSV from the GPU for
   every strategy
+* ``fodeabm.checks.check_strategy_equivalence`` (checks.py:144-168) also
+  checks ``gpu`` against ``solve_serial`` on its power-law problem, so
+  ``fodeabm verify`` covers the GPU strategy with the reference's tolerance
 
 Problems built with the reference's own rhs factories run unchanged (see
 :func:`paper_1611_08678_b200.systems.adopt_reference_rhs`).  ``uninstall()``
@@ -36,6 +39,7 @@ def install(weights: str = "accurate"):
     fodeabm = importlib.import_module("fodeabm")
     bench = importlib.import_module("fodeabm.bench")
     cli = importlib.import_module("fodeabm.cli")
+    checks = importlib.import_module("fodeabm.checks")
     if _SAVED:
         return fodeabm
     _SAVED["STRATEGIES"] = bench.STRATEGIES
@@ -43,6 +47,8 @@ def install(weights: str = "accurate"):
     _SAVED["solve_with_strategy"] = cli.solve_with_strategy
     _SAVED["_build_parser"] = cli._build_parser
     _SAVED["write_trajectory_csv"] = cli.write_trajectory_csv
+    _SAVED["check_strategy_equivalence"] = checks.check_strategy_equivalence
+    orig_equiv = checks.check_strategy_equivalence
     orig_once = bench._solve_once
     orig_solve = cli.solve_with_strategy
     orig_parser = cli._build_parser
@@ -64,11 +70,21 @@ def install(weights: str = "accurate"):
                 action.choices = (*action.choices, STRATEGY_NAME)
         return parser
 
+    def check_strategy_equivalence(n_steps=2048, n_workers=2, chunk=1024):
+        out = orig_equiv(n_steps, n_workers, chunk)
+        problem = checks._power_problem(0.5)
+        grid = problem.grid(n_steps)
+        ref = checks.solve_serial(problem, grid)
+        dev = checks._sup_rel_dev(solve_gpu(problem, grid, weights=weights), ref)
+        out.append(checks.CheckResult(f"{STRATEGY_NAME} strategy", dev <= checks.EQUIV_TOL, f"sup rel dev {dev:.3e}"))
+        return out
+
     bench.STRATEGIES = (*bench.STRATEGIES, STRATEGY_NAME)
     bench._solve_once = _solve_once
     cli.solve_with_strategy = solve_with_strategy
     cli._build_parser = _build_parser
     cli.write_trajectory_csv = write_trajectory_csv
+    checks.check_strategy_equivalence = check_strategy_equivalence
     return fodeabm
 
 
@@ -82,6 +98,7 @@ def uninstall():
     cli.solve_with_strategy = _SAVED["solve_with_strategy"]
     cli._build_parser = _SAVED["_build_parser"]
     cli.write_trajectory_csv = _SAVED["write_trajectory_csv"]
+    importlib.import_module("fodeabm.checks").check_strategy_equivalence = _SAVED["check_strategy_equivalence"]
     _SAVED.clear()
 
 

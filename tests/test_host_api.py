@@ -230,6 +230,17 @@ class TestStrategyPlugin:
         from paper_1611_08678_b200.output import write_trajectory_csv as device_writer
 
         assert cli.write_trajectory_csv is device_writer
+        # fodeabm verify's equivalence check gains the gpu strategy (checks.py:144-168)
+        import fodeabm.checks as checks
+        from paper_1611_08678_b200 import strategy as strat
+
+        fake = strat.solve_gpu
+        strat.solve_gpu = lambda problem, grid, **kw: checks.solve_serial(problem, grid)
+        try:
+            res = checks.check_strategy_equivalence(n_steps=64, n_workers=1)
+        finally:
+            strat.solve_gpu = fake
+        assert res[-1].name == "gpu strategy" and res[-1].passed
         # other strategies still reach the reference implementations
         traj = bench._solve_once(problem, "serial", 16, 1, 1024)
         assert traj.states.shape == (17, 1)
