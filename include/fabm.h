@@ -239,6 +239,24 @@ int fabm_mittag_leffler(const double* alpha, const double* z, int64_t n,
                         int device, double* out, int32_t* codes,
                         fabm_status* status);
 
+/* ---- single-step ops: replace step_predictor / step_corrector ------------
+ * (serial.py:74-111).  For each requested step index ns[i] (0 <= n <
+ * grid.n_steps), from the prefix f_cache[0..n] (host, n_rows x dim):
+ *   yp_out[i] = y0 + h^a * sum_{k<=n} b_{n-k} f_k                 (predictor)
+ *   y_out[i]  = y0 + h^a * ((c_n f_0 + sum_{1<=k<=n} a_{n-k} f_k)
+ *                           + f(t_{n+1}, y_pred[i]) / Gamma(a+2)) (corrector)
+ * y_pred NULL uses the computed predictor (one full PECE step).  b/a/c hold
+ * n_weights entries (a WeightTable).  err_out[i]: 0 ok; 1 the predicted state
+ * is non-finite; 2 the rhs returned a non-finite value (both are the
+ * reference's SolverStepError(step=n, t=(n+1)h); y_out is nan there).  An
+ * index out of range is FABM_ERR_CONFIG (the reference's ValueError). */
+int fabm_step_pc(const fabm_problem* problem, const fabm_grid* grid,
+                 const double* b, const double* a, const double* c,
+                 int64_t n_weights, const double* f_cache, int64_t n_rows,
+                 const int64_t* ns, int64_t count, const double* y_pred,
+                 double* yp_out, double* y_out, int32_t* err_out, int device,
+                 fabm_status* status);
+
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
 /* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */
 double fabm_measure_dfma_peak(int device);

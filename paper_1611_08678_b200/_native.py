@@ -61,6 +61,7 @@ EXPORTED_SYMBOLS = (
     "fabm_write_csv",
     "fabm_plan_write_csv",
     "fabm_mittag_leffler",
+    "fabm_step_pc",
 )
 
 
@@ -149,6 +150,9 @@ def _declare(lib):
         "fabm_write_csv": (ctypes.c_int, [ctypes.c_char_p, _DP, _DP, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
                                           ctypes.c_int, _I64P, _DP, S]),
         "fabm_plan_write_csv": (ctypes.c_int, [plan, ctypes.c_char_p, _I64P, _DP, S]),
+        "fabm_step_pc": (ctypes.c_int, [P, G, _DP, _DP, _DP, ctypes.c_int64, _DP, ctypes.c_int64, _I64P,
+                                        ctypes.c_int64, _DP, _DP, _DP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int,
+                                        S]),
         "fabm_mittag_leffler": (ctypes.c_int, [_DP, _DP, ctypes.c_int64, ctypes.c_int, _DP,
                                                ctypes.POINTER(ctypes.c_int32), S]),
     }

@@ -19,6 +19,7 @@
 #include "batch.cuh"
 #include "csv_format.cuh"
 #include "oracles.cuh"
+#include "steps.cuh"
 #include "engine.cuh"
 #include "weights.cuh"
 
@@ -94,6 +95,35 @@ void fill_scalars(const fabm_problem* p, fabm_grid* g) {
   if (g->inv_gamma2 == 0.0) g->inv_gamma2 = 1.0 / g->gamma2;
 }
 
+// (system, dim) -> the LAUNCHER<SYS, D> instantiation compiled for it (every
+// device rhs: constant/linear for d <= 4, the named systems at their dims)
+#define FABM_PICK_SYSTEM(LAUNCHER)                                   \
+  switch (sys) {                                                     \
+    case FABM_SYS_CONSTANT:                                          \
+      switch (dim) {                                                 \
+        case 1: return LAUNCHER<SYS_CONSTANT, 1>;                    \
+        case 2: return LAUNCHER<SYS_CONSTANT, 2>;                    \
+        case 3: return LAUNCHER<SYS_CONSTANT, 3>;                    \
+        case 4: return LAUNCHER<SYS_CONSTANT, 4>;                    \
+      }                                                              \
+      break;                                                         \
+    case FABM_SYS_LINEAR:                                            \
+      switch (dim) {                                                 \
+        case 1: return LAUNCHER<SYS_LINEAR, 1>;                      \
+        case 2: return LAUNCHER<SYS_LINEAR, 2>;                      \
+        case 3: return LAUNCHER<SYS_LINEAR, 3>;                      \
+        case 4: return LAUNCHER<SYS_LINEAR, 4>;                      \
+      }                                                              \
+      break;                                                         \
+    case FABM_SYS_POWER_LAW: return LAUNCHER<SYS_POWER_LAW, 1>;      \
+    case FABM_SYS_HINDMARSH_ROSE: return LAUNCHER<SYS_HINDMARSH_ROSE, 3>; \
+    case FABM_SYS_LORENZ: return LAUNCHER<SYS_LORENZ, 3>;            \
+    case FABM_SYS_CHEN: return LAUNCHER<SYS_CHEN, 3>;                \
+    case FABM_SYS_ROSSLER: return LAUNCHER<SYS_ROSSLER, 3>;          \
+    case FABM_SYS_FINANCIAL: return LAUNCHER<SYS_FINANCIAL, 3>;      \
+  }                                                                  \
+  return nullptr
+
 using EngineLaunch = cudaError_t (*)(const EngineParams&, int grid, cudaStream_t);
 
 template <int SYS, int D>
@@ -117,31 +147,7 @@ cudaError_t engine_occupancy(int* blocks_per_sm) {
 }
 
 EngineLaunch pick_engine(int sys, int dim) {
-  switch (sys) {
-    case FABM_SYS_CONSTANT:
-      switch (dim) {
-        case 1: return launch_engine<SYS_CONSTANT, 1>;
-        case 2: return launch_engine<SYS_CONSTANT, 2>;
-        case 3: return launch_engine<SYS_CONSTANT, 3>;
-        case 4: return launch_engine<SYS_CONSTANT, 4>;
-      }
-      break;
-    case FABM_SYS_LINEAR:
-      switch (dim) {
-        case 1: return launch_engine<SYS_LINEAR, 1>;
-        case 2: return launch_engine<SYS_LINEAR, 2>;
-        case 3: return launch_engine<SYS_LINEAR, 3>;
-        case 4: return launch_engine<SYS_LINEAR, 4>;
-      }
-      break;
-    case FABM_SYS_POWER_LAW: return launch_engine<SYS_POWER_LAW, 1>;
-    case FABM_SYS_HINDMARSH_ROSE: return launch_engine<SYS_HINDMARSH_ROSE, 3>;
-    case FABM_SYS_LORENZ: return launch_engine<SYS_LORENZ, 3>;
-    case FABM_SYS_CHEN: return launch_engine<SYS_CHEN, 3>;
-    case FABM_SYS_ROSSLER: return launch_engine<SYS_ROSSLER, 3>;
-    case FABM_SYS_FINANCIAL: return launch_engine<SYS_FINANCIAL, 3>;
-  }
-  return nullptr;
+  FABM_PICK_SYSTEM(launch_engine);
 }
 
 int stride_of(int dim) { return dim == 1 ? 1 : (dim == 2 ? 2 : 4); }
@@ -697,31 +703,7 @@ cudaError_t launch_batch(const BatchParams& P, int grid, cudaStream_t stream) {
 }
 
 BatchLaunch pick_batch(int sys, int dim) {
-  switch (sys) {
-    case FABM_SYS_CONSTANT:
-      switch (dim) {
-        case 1: return launch_batch<SYS_CONSTANT, 1>;
-        case 2: return launch_batch<SYS_CONSTANT, 2>;
-        case 3: return launch_batch<SYS_CONSTANT, 3>;
-        case 4: return launch_batch<SYS_CONSTANT, 4>;
-      }
-      break;
-    case FABM_SYS_LINEAR:
-      switch (dim) {
-        case 1: return launch_batch<SYS_LINEAR, 1>;
-        case 2: return launch_batch<SYS_LINEAR, 2>;
-        case 3: return launch_batch<SYS_LINEAR, 3>;
-        case 4: return launch_batch<SYS_LINEAR, 4>;
-      }
-      break;
-    case FABM_SYS_POWER_LAW: return launch_batch<SYS_POWER_LAW, 1>;
-    case FABM_SYS_HINDMARSH_ROSE: return launch_batch<SYS_HINDMARSH_ROSE, 3>;
-    case FABM_SYS_LORENZ: return launch_batch<SYS_LORENZ, 3>;
-    case FABM_SYS_CHEN: return launch_batch<SYS_CHEN, 3>;
-    case FABM_SYS_ROSSLER: return launch_batch<SYS_ROSSLER, 3>;
-    case FABM_SYS_FINANCIAL: return launch_batch<SYS_FINANCIAL, 3>;
-  }
-  return nullptr;
+  FABM_PICK_SYSTEM(launch_batch);
 }
 
 struct DevBuf {
@@ -1219,5 +1201,98 @@ extern "C" int fabm_mittag_leffler(const double* alpha, const double* z, int64_t
     set_status(status, FABM_ERR_CUDA, "mittag_leffler: %s", cudaGetErrorString(e));
     return FABM_ERR_CUDA;
   }
+  return FABM_OK;
+}
+
+// ======================================================================
+// Single-step ops (serial.py:74-111) — steps.cuh
+// ======================================================================
+namespace {
+using StepLaunch = cudaError_t (*)(const StepParams&, cudaStream_t);
+template <int SYS, int D>
+cudaError_t launch_steps(const StepParams& P, cudaStream_t stream) {
+  const long long blocks = (P.count + 7) / 8;  // 8 warps (requests) per CTA
+  step_pc_kernel<SYS, D><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+StepLaunch pick_steps(int sys, int dim) { FABM_PICK_SYSTEM(launch_steps); }
+}  // namespace
+
+extern "C" int fabm_step_pc(const fabm_problem* problem, const fabm_grid* grid, const double* b, const double* a,
+                            const double* c, int64_t n_weights, const double* f_cache, int64_t n_rows,
+                            const int64_t* ns, int64_t count, const double* y_pred, double* yp_out, double* y_out,
+                            int32_t* err_out, int device, fabm_status* status) {
+  clear_status(status);
+  if (!problem || !grid || !b || !a || !c || !f_cache || (count > 0 && (!ns || !err_out)) || count < 0) {
+    set_status(status, FABM_ERR_CONFIG, "step_pc: null argument");
+    return FABM_ERR_CONFIG;
+  }
+  const int d = problem->dim;
+  StepLaunch launch = pick_steps(problem->system, d);
+  if (!launch) {
+    set_status(status, FABM_ERR_CONFIG, "no device rhs for system %d with dim %d", problem->system, d);
+    return FABM_ERR_CONFIG;
+  }
+  long long nmax = -1;
+  for (int64_t i = 0; i < count; ++i) {
+    const long long n = ns[i];
+    // _history_transposed, serial.py:67-71
+    if (n < 0 || n >= grid->n_steps) {
+      set_status(status, FABM_ERR_CONFIG, "step index n=%lld outside [0, %lld)", n,
+                 static_cast<long long>(grid->n_steps));
+      return FABM_ERR_CONFIG;
+    }
+    if (n >= n_rows || n >= n_weights) {
+      set_status(status, FABM_ERR_CONFIG, "step index n=%lld needs %lld f rows and weights (have %lld, %lld)", n,
+                 n + 1, static_cast<long long>(n_rows), static_cast<long long>(n_weights));
+      return FABM_ERR_CONFIG;
+    }
+    nmax = std::max(nmax, n);
+  }
+  if (count == 0) return FABM_OK;
+  const int ndev = fabm_device_count();
+  if (ndev <= 0 || device < 0 || device >= ndev) {
+    set_status(status, FABM_ERR_NODEVICE, "no CUDA device %d (found %d)", device, ndev);
+    return FABM_ERR_NODEVICE;
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  fabm_grid g = *grid;
+  fill_scalars(problem, &g);
+  const size_t nw = static_cast<size_t>(nmax + 1), nq = static_cast<size_t>(count);
+  DevBuf buf;
+  const size_t bytes = sizeof(double) * (3 * nw + nw * d + d + 3 * nq * d) + sizeof(long long) * nq + sizeof(int) * nq;
+  CUDA_TRY(cudaMalloc(&buf.p, bytes));
+  double* w = buf.as<double>();
+  StepParams P{};
+  P.count = count;
+  P.wb = w;
+  P.wa = w + nw;
+  P.wc = w + 2 * nw;
+  P.F = w + 3 * nw;
+  double* y0 = w + 3 * nw + nw * d;
+  double* yq = y0 + d;
+  P.y0 = y0;
+  P.yp_out = yq + nq * d;
+  P.y_out = yq + 2 * nq * d;
+  P.ypred = y_pred ? yq : nullptr;
+  long long* dns = reinterpret_cast<long long*>(yq + 3 * nq * d);
+  P.ns = dns;
+  P.err = reinterpret_cast<int*>(dns + nq);
+  P.h = g.h;
+  P.ha = g.h_alpha;
+  P.ig = g.inv_gamma2;
+  std::memcpy(P.params, problem->params, sizeof(P.params));
+  CUDA_TRY(cudaMemcpy(w, b, sizeof(double) * nw, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(w + nw, a, sizeof(double) * nw, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(w + 2 * nw, c, sizeof(double) * nw, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(w + 3 * nw, f_cache, sizeof(double) * nw * d, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(y0, problem->y0, sizeof(double) * d, cudaMemcpyHostToDevice));
+  if (y_pred) CUDA_TRY(cudaMemcpy(yq, y_pred, sizeof(double) * nq * d, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dns, ns, sizeof(long long) * nq, cudaMemcpyHostToDevice));
+  CUDA_TRY(launch(P, nullptr));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (yp_out) CUDA_TRY(cudaMemcpy(yp_out, P.yp_out, sizeof(double) * nq * d, cudaMemcpyDeviceToHost));
+  if (y_out) CUDA_TRY(cudaMemcpy(y_out, P.y_out, sizeof(double) * nq * d, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(err_out, P.err, sizeof(int) * nq, cudaMemcpyDeviceToHost));
   return FABM_OK;
 }
