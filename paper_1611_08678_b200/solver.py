@@ -50,8 +50,11 @@ def _raise_status(st: nat.Status, h: float | None = None):
     msg = st.message.decode(errors="replace")
     if st.code == nat.FABM_ERR_NONFINITE:
         if st.kind == 1:
-            raise SolverStepError("rhs returned a non-finite value", step=0, t=0.0)
-        raise SolverStepError("rhs returned a non-finite value", step=int(st.step), t=float(st.t))
+            exc = SolverStepError("rhs returned a non-finite value", step=0, t=0.0)
+        else:
+            exc = SolverStepError("rhs returned a non-finite value", step=int(st.step), t=float(st.t))
+        exc.kind = int(st.kind)
+        raise exc
     if st.code == nat.FABM_ERR_TIMEOUT:
         raise StrategyTimeoutError(msg or "device watchdog expired")
     if st.code == nat.FABM_ERR_CONFIG:
@@ -65,7 +68,8 @@ def _structs(problem, grid):
     if tag.dim is not None and tag.dim != dim:
         raise ValueError(f"rhs {tag.name!r} has dimension {tag.dim}, problem has dim {dim}")
     if dim > nat.MAX_DIM:
-        raise ValueError(f"the device engine supports dim <= {nat.MAX_DIM}, got {dim}")
+        raise ValueError(f"the device engine supports dim <= {nat.MAX_DIM} for {tag.name!r} (solve_gpu splits "
+                         f"the componentwise constant/linear systems of any dim), got {dim}")
     alpha = float(problem.alpha)
     pr = nat.Problem()
     pr.alpha = alpha
@@ -272,9 +276,12 @@ def solve_gpu(
     N = int(grid.n_steps)
     if not grid.spans(problem.t_end):
         raise ValueError(f"grid (h={grid.h!r}, N={N}) does not span t_end={problem.t_end!r}")
-    device_system_of(problem.rhs)
+    tag = device_system_of(problem.rhs)
     # shape and finiteness of f(0, y0), exactly as the reference validates it
     problem.eval_rhs0()
+    if int(problem.dim) > nat.MAX_DIM and tag.name in COMPONENTWISE:
+        return _solve_by_components(problem, grid, tag, weights=weights, device=device, timeout_s=timeout_s,
+                                    stats=stats)
     cached = _PLAN_CACHE_SIZE and isinstance(weights, str)
     plan = _cached_plan(problem, grid, weights, device)
     if cached:
@@ -288,6 +295,51 @@ def solve_gpu(
         stats.update(plan.stats())
         stats["strategy"] = STRATEGY_NAME
     return traj
+
+
+# systems whose components evolve independently: f_i depends on y_i only
+# (constant: f = value, systems.py:26-36; linear: f = lam * y, :64-73)
+COMPONENTWISE = ("constant", "linear")
+
+
+def _component_problem(problem, tag, lo: int, hi: int):
+    from .core import FractionalProblem
+    from .systems import rhs_constant, rhs_linear
+
+    rhs = rhs_constant(tag.params[lo:hi]) if tag.name == "constant" else rhs_linear(tag.params[0])
+    return FractionalProblem(alpha=problem.alpha, dim=hi - lo, rhs=rhs, y0=problem.y0[lo:hi], t_end=problem.t_end)
+
+
+def _solve_by_components(problem, grid, tag, **kw) -> Trajectory:
+    """dim > MAX_DIM for a componentwise rhs: solve blocks of <= MAX_DIM
+    components with the engine and join them.  Every component's arithmetic
+    is independent of the others (history sums, assembly and rhs are all
+    per component), so this is the d-dimensional solve; a non-finite value
+    raises at the earliest failing step over all blocks, as the reference's
+    whole-vector check does (serial.py:157,167)."""
+    dim = int(problem.dim)
+    stats = kw.pop("stats", None)
+    states, f_cache, first = [], [], None
+    kernel_ms = 0.0
+    for lo in range(0, dim, nat.MAX_DIM):
+        hi = min(dim, lo + nat.MAX_DIM)
+        sub = {}
+        try:
+            tr = solve_gpu(_component_problem(problem, tag, lo, hi), grid, stats=sub, **kw)
+        except SolverStepError as exc:
+            key = (exc.step, getattr(exc, "kind", 3))
+            if first is None or key < (first.step, getattr(first, "kind", 3)):
+                first = exc
+            continue
+        kernel_ms += sub.get("kernel_ms", 0.0)
+        states.append(tr.states)
+        f_cache.append(tr.f_cache)
+    if first is not None:
+        raise first
+    if stats is not None:
+        stats.update(kernel_ms=kernel_ms, strategy=STRATEGY_NAME, component_blocks=len(states))
+    g = grid if isinstance(grid, GridSpec) else GridSpec(grid.n_steps, grid.h)
+    return Trajectory(grid=g, states=np.concatenate(states, axis=1), f_cache=np.concatenate(f_cache, axis=1))
 
 
 class BatchResult:

@@ -218,3 +218,41 @@ def test_power_law_device_rhs_bitwise(fabm):
     host = np.array([rhs(ti, None)[0] for ti in grid.times()])
     # CUDA pow vs libm pow may differ by an ulp; the reference tolerance is 1e-14 here
     np.testing.assert_allclose(traj.f_cache[:, 0], host, rtol=2e-16 * 4, atol=0)
+
+
+# ---- dim > 4: componentwise systems are solved in blocks of <= 4 components
+def test_componentwise_high_dim_matches_oracle_and_1d_solves(fabm):
+    rng = np.random.default_rng(5)
+    d = 6
+    y0 = rng.uniform(-2.0, 2.0, size=d)
+    problem = fabm.FractionalProblem(alpha=0.7, dim=d, rhs=fabm.rhs_linear(-0.8), y0=y0, t_end=5.0)
+    grid = problem.grid(3000)
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    ref_states, _ = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, grid.n_steps)
+    assert normwise_dev(traj.states, ref_states) <= 1e-12
+    # each component is exactly its own 1-D solve (the engine's arithmetic is per component)
+    for i in range(d):
+        p1 = fabm.FractionalProblem(alpha=0.7, dim=1, rhs=fabm.rhs_linear(-0.8), y0=[y0[i]], t_end=5.0)
+        assert np.array_equal(fabm.solve_gpu(p1, grid, weights="reference").states[:, 0], traj.states[:, i])
+
+
+def test_componentwise_constant_dim_20(fabm):
+    vals = np.linspace(-3.0, 3.0, 20)
+    problem = fabm.FractionalProblem(alpha=0.5, dim=20, rhs=fabm.rhs_constant(vals), y0=np.zeros(20), t_end=1.0)
+    grid = problem.grid(500)
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    ref_states, ref_f = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, grid.n_steps)
+    assert normwise_dev(traj.states, ref_states) <= 1e-12
+    assert np.array_equal(traj.f_cache, ref_f)
+
+
+def test_componentwise_high_dim_error_is_earliest_step(fabm):
+    y0 = np.array([1.0, 1.0, 1.0, 1.0, 1e300, 1.0])
+    problem = fabm.FractionalProblem(alpha=1.0, dim=6, rhs=fabm.rhs_linear(80.0), y0=y0, t_end=10.0)
+    grid = problem.grid(1000)
+    p1 = fabm.FractionalProblem(alpha=1.0, dim=1, rhs=fabm.rhs_linear(80.0), y0=[1e300], t_end=10.0)
+    with pytest.raises(fabm.SolverStepError) as e1:
+        fabm.solve_gpu(p1, grid)
+    with pytest.raises(fabm.SolverStepError) as e6:
+        fabm.solve_gpu(problem, grid)
+    assert (e6.value.step, e6.value.t) == (e1.value.step, e1.value.t)
