@@ -244,11 +244,23 @@ __device__ __forceinline__ int format_g17(double v, char* out) {
   unsigned long long D;
   int X;
   decimal17(m, e, &D, &X);
+  // 17 digits as 1 + 8 + 8: one 64-bit split, then 32-bit arithmetic
   char dg[17];
+  const unsigned long long top = D / 100000000ull;  // < 10^9
+  uint32_t lo = static_cast<uint32_t>(D - top * 100000000ull);
+  uint32_t mid = static_cast<uint32_t>(top % 100000000ull);
+  dg[0] = static_cast<char>('0' + static_cast<uint32_t>(top / 100000000ull));
 #pragma unroll
-  for (int i = 16; i >= 0; --i) {
-    dg[i] = static_cast<char>('0' + D % 10ull);
-    D /= 10ull;
+  for (int i = 8; i >= 1; --i) {
+    const uint32_t q = mid / 10u;
+    dg[i] = static_cast<char>('0' + (mid - 10u * q));
+    mid = q;
+  }
+#pragma unroll
+  for (int i = 16; i >= 9; --i) {
+    const uint32_t q = lo / 10u;
+    dg[i] = static_cast<char>('0' + (lo - 10u * q));
+    lo = q;
   }
   int nd = 17;
   while (nd > 1 && dg[nd - 1] == '0') --nd;

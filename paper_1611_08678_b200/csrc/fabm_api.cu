@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cerrno>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1017,6 +1018,10 @@ int csv_format_device(const double* d_states, const double* d_t, double h, long 
   return FABM_OK;
 }
 
+constexpr long long kCsvStageBytes = 32ll << 20;
+std::mutex g_csv_stage_mu;
+char* g_csv_stage[2] = {nullptr, nullptr};
+
 // Device bytes -> file, through two pinned staging buffers so the D2H of
 // chunk i+1 overlaps the write of chunk i.
 int csv_write_file(const char* path, const char* d_bytes, long long n, cudaStream_t stream, fabm_status* status) {
@@ -1026,8 +1031,11 @@ int csv_write_file(const char* path, const char* d_bytes, long long n, cudaStrea
     set_status(status, FABM_ERR_IO, "%s: %s", path, std::strerror(errno));
     return FABM_ERR_IO;
   }
-  constexpr long long kChunk = 32ll << 20;
-  char* pin[2] = {nullptr, nullptr};
+  constexpr long long kChunk = kCsvStageBytes;
+  // the pinned staging pair is allocated once per process (cudaMallocHost
+  // costs milliseconds) and serialised by a mutex
+  std::lock_guard<std::mutex> lock(g_csv_stage_mu);
+  char** pin = g_csv_stage;
   cudaEvent_t done[2] = {nullptr, nullptr};
   int rc = FABM_OK;
   auto fail_cuda = [&](const char* what, cudaError_t e) {
@@ -1036,7 +1044,7 @@ int csv_write_file(const char* path, const char* d_bytes, long long n, cudaStrea
   };
   cudaError_t e;
   for (int i = 0; i < 2 && rc == FABM_OK; ++i) {
-    if ((e = cudaMallocHost(&pin[i], kChunk)) != cudaSuccess) fail_cuda("cudaMallocHost", e);
+    if (!pin[i] && (e = cudaMallocHost(&pin[i], kChunk)) != cudaSuccess) fail_cuda("cudaMallocHost", e);
     else if ((e = cudaEventCreate(&done[i])) != cudaSuccess) fail_cuda("cudaEventCreate", e);
   }
   const long long n_chunks = (n + kChunk - 1) / kChunk;
@@ -1061,10 +1069,8 @@ int csv_write_file(const char* path, const char* d_bytes, long long n, cudaStrea
     set_status(status, FABM_ERR_IO, "%s: %s", path, std::strerror(errno));
     rc = FABM_ERR_IO;
   }
-  for (int i = 0; i < 2; ++i) {
-    if (pin[i]) cudaFreeHost(pin[i]);
+  for (int i = 0; i < 2; ++i)
     if (done[i]) cudaEventDestroy(done[i]);
-  }
   return rc;
 }
 

@@ -70,13 +70,22 @@ def _check_path(path):
     return p
 
 
+_SCRATCH = [np.empty(0, dtype=np.uint8)]
+
+
+def _scratch(n: int) -> np.ndarray:
+    if _SCRATCH[0].shape[0] < n:
+        _SCRATCH[0] = np.empty(max(n, 1), dtype=np.uint8)
+    return _SCRATCH[0]
+
+
 def format_trajectory_csv(traj, *, device: int = 0, stats: dict | None = None) -> bytes:
     """The bytes ``write_trajectory_csv`` would write (cli.py:97-105)."""
     lib = nat.load()
     states, t = _arrays(traj)
     n_rows, dim = states.shape
     cap = csv_upper_bound(n_rows, dim)
-    buf = np.empty(max(cap, 1), dtype=np.uint8)  # not zero-filled: the library writes every byte it reports
+    buf = _scratch(cap)  # reused between calls (already faulted in); the library writes every byte it reports
     n = ctypes.c_int64(0)
     ms = ctypes.c_double(0.0)
     st = nat.Status()
