@@ -93,7 +93,7 @@ struct EngineParams {
   int n_agents;            // bulk agents = 16 * (gridDim.x - 1)
   unsigned long long timeout_ns;
   unsigned long long* trace;  // FABM_PROFILE: per block {src published, ready, staged, first need}
-  int debug;               // dev experiments: 1 = leader alone (results invalid)
+  int debug;               // dev experiments: 1 = leader alone, 8 = no bulk agents (results invalid)
   // sharding (config 5).  n_shards = 1: everything local.  my_shard >= 0: this
   // launch hosts the agents of that shard (and the stepper if it is 0);
   // my_shard = -1: one-GPU emulation, agent CTA b belongs to shard (b-1) % n_shards
@@ -935,7 +935,7 @@ template <int D>
 __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
-  if (agent >= n_targets) return;
+  if (agent >= n_targets || (P.debug & 8)) return;  // debug 8 (dev): no bulk agents (results invalid)
   const int nA = P.n_agents;
   const int nown = owned_count(agent, nA, n_targets);
   if (nown == 0) return;

@@ -256,3 +256,22 @@ def test_componentwise_high_dim_error_is_earliest_step(fabm):
     with pytest.raises(fabm.SolverStepError) as e6:
         fabm.solve_gpu(problem, grid)
     assert (e6.value.step, e6.value.t) == (e1.value.step, e1.value.t)
+
+
+def test_watchdog_raises_strategy_timeout(fabm, monkeypatch):
+    # dev switch 8 keeps the bulk agents idle, so the stepper waits for target
+    # sums that never come: the device watchdog must fire (the reference's
+    # StrategyTimeoutError, _shm.py:115-116) and leave the GPU usable
+    import time
+
+    problem = fabm.FractionalProblem(alpha=0.9, dim=3, rhs=fabm.rhs_lorenz(), y0=(1.0, 1.0, 1.0), t_end=1.0)
+    grid = problem.grid(5000)
+    monkeypatch.setenv("FABM_DEBUG_MODE", "8")
+    t0 = time.perf_counter()
+    with pytest.raises(fabm.StrategyTimeoutError):
+        fabm.solve_gpu(problem, grid, timeout_s=0.5)
+    assert time.perf_counter() - t0 < 30.0
+    monkeypatch.delenv("FABM_DEBUG_MODE")
+    traj = fabm.solve_gpu(problem, grid, weights="reference")
+    ref_states, _ = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, grid.n_steps)
+    assert normwise_dev(traj.states, ref_states) <= 1e-12
