@@ -295,7 +295,10 @@ def run_fabm(args, world, rank, local):
     times = []
     h2d = 8 * 3 + 8 * 16  # y0 + rhs params
     d2h = 2 * (n + 1) * 3 * 8  # states + f_cache
-    fabm.solve_gpu(problem, grid)  # warm plan cache
+    # warm the plan cache and the pinned output pool: a loop `traj = solve_gpu(...)`
+    # holds the previous trajectory while the next one streams in (two buffer sets)
+    warm = [fabm.solve_gpu(problem, grid) for _ in range(2)]
+    del warm
     barrier(world)
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()

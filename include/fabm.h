@@ -161,6 +161,16 @@ int fabm_plan_download_last(fabm_plan* plan, double* y_last, fabm_status* status
 int fabm_plan_stats(const fabm_plan* plan, fabm_stats* stats);
 void fabm_plan_destroy(fabm_plan* plan);
 
+/* Stream the next runs' trajectory (states, f_cache: (n_steps+1)*dim doubles
+ * each) straight into pinned host memory while the kernel runs, so no D2H
+ * copy follows the solve.  The buffers must be mapped pinned memory, e.g.
+ * from fabm_host_alloc, and stay valid until the plan is reset with NULLs or
+ * destroyed.  Both NULL: back to device-only output (fabm_plan_download). */
+int fabm_plan_set_host_output(fabm_plan* plan, double* states, double* f_cache,
+                              fabm_status* status);
+void* fabm_host_alloc(int64_t bytes);   /* mapped, portable pinned memory; NULL on failure */
+void fabm_host_free(void* ptr);
+
 /* Zero the run flags of a plan.  fabm_plan_run does this itself, except on a
  * plan attached to peer shards: there every rank calls fabm_plan_reset, then
  * the ranks barrier, then every rank calls fabm_plan_run. */

@@ -62,6 +62,9 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_write_csv",
     "fabm_mittag_leffler",
     "fabm_step_pc",
+    "fabm_plan_set_host_output",
+    "fabm_host_alloc",
+    "fabm_host_free",
 )
 
 
@@ -150,6 +153,9 @@ def _declare(lib):
         "fabm_write_csv": (ctypes.c_int, [ctypes.c_char_p, _DP, _DP, ctypes.c_int64, ctypes.c_int32, ctypes.c_double,
                                           ctypes.c_int, _I64P, _DP, S]),
         "fabm_plan_write_csv": (ctypes.c_int, [plan, ctypes.c_char_p, _I64P, _DP, S]),
+        "fabm_plan_set_host_output": (ctypes.c_int, [plan, _DP, _DP, S]),
+        "fabm_host_alloc": (ctypes.c_void_p, [ctypes.c_int64]),
+        "fabm_host_free": (None, [ctypes.c_void_p]),
         "fabm_step_pc": (ctypes.c_int, [P, G, _DP, _DP, _DP, ctypes.c_int64, _DP, ctypes.c_int64, _I64P,
                                         ctypes.c_int64, _DP, _DP, _DP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int,
                                         S]),

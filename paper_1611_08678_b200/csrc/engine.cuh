@@ -85,6 +85,8 @@ struct EngineParams {
   double* Y;               // states (N+1) x d
   double* F;               // f history (nb*B + B) x DS
   double* Fc;              // f_cache output, (N+1) x d compact
+  double* Yh;              // optional: states / f_cache also streamed to mapped
+  double* Fch;             //   pinned host memory (device aliases), or null
   double* BK;              // bulk accumulators (nb*B) x 2 x DS
   int* ready;              // per target block: bulk complete
   DevCtrl* ctrl;
@@ -681,6 +683,12 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
       double* fo = P.Fc + k * D;
 #pragma unroll
       for (int c = 0; c < D; ++c) { yd[c] = yf[c]; fd[c] = yf[D + c]; fo[c] = yf[D + c]; }
+      if (P.Yh) {  // trajectory streamed to mapped pinned host memory during the run (no D2H afterwards)
+        double* yh = P.Yh + k * D;
+        double* fh = P.Fch + k * D;
+#pragma unroll
+        for (int c = 0; c < D; ++c) { yh[c] = yf[c]; fh[c] = yf[D + c]; }
+      }
       for (int sh = 1; sh < P.n_shards; ++sh) {  // peer copies of the f history
         double* fp = P.shard[sh].F + k * DS;
 #pragma unroll

@@ -187,6 +187,8 @@ struct fabm_plan {
   double* y0 = nullptr;
   double* Y = nullptr;
   double* Fc = nullptr;
+  double* Yh = nullptr;    // device aliases of the caller's mapped pinned output (fabm_plan_set_host_output)
+  double* Fch = nullptr;
   // the shard arena: {ctrl, ready, F, BK} in one allocation so that one CUDA
   // IPC handle exposes it to the peer GPUs of a sharded run (config 5)
   char* arena = nullptr;
@@ -409,6 +411,8 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   P.Y = p->Y;
   P.F = p->F;
   P.Fc = p->Fc;
+  P.Yh = p->Yh;
+  P.Fch = p->Fch;
   P.BK = p->BK;
   P.ready = p->ready;
   P.ctrl = p->ctrl;
@@ -1302,3 +1306,50 @@ extern "C" int fabm_step_pc(const fabm_problem* problem, const fabm_grid* grid, 
   CUDA_TRY(cudaMemcpy(err_out, P.err, sizeof(int) * nq, cudaMemcpyDeviceToHost));
   return FABM_OK;
 }
+
+// ======================================================================
+// Pinned host output (the trajectory streamed to the host during the run)
+// ======================================================================
+extern "C" {
+
+void* fabm_host_alloc(int64_t bytes) {
+  void* ptr = nullptr;
+  if (bytes <= 0) return nullptr;
+  if (cudaHostAlloc(&ptr, static_cast<size_t>(bytes), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+    return nullptr;
+  return ptr;
+}
+
+void fabm_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
+int fabm_plan_set_host_output(fabm_plan* p, double* states, double* f_cache, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if ((states == nullptr) != (f_cache == nullptr)) {
+    set_status(status, FABM_ERR_CONFIG, "host output needs both states and f_cache (or neither)");
+    return FABM_ERR_CONFIG;
+  }
+  if (p->n_shards > 1 && !p->virt && p->rank != 0) {
+    set_status(status, FABM_ERR_CONFIG, "host output lives on the stepper's rank (0)");
+    return FABM_ERR_CONFIG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  p->Yh = p->Fch = nullptr;
+  if (!states) return FABM_OK;
+  void *dy = nullptr, *df = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dy, states, 0);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&df, f_cache, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_status(status, FABM_ERR_CONFIG, "host output must be mapped pinned memory (fabm_host_alloc): %s",
+               cudaGetErrorString(e));
+    return FABM_ERR_CONFIG;
+  }
+  p->Yh = static_cast<double*>(dy);
+  p->Fch = static_cast<double*>(df);
+  return FABM_OK;
+}
+
+}  // extern "C"

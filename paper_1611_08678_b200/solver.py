@@ -193,6 +193,31 @@ class GpuPlan:
             _raise_status(st, self.grid.h)
         return self.stats()["kernel_ms"]
 
+    def set_host_output(self, states: np.ndarray | None, f_cache: np.ndarray | None):
+        """Stream the next run's trajectory into these mapped pinned arrays (None: off)."""
+        st = nat.Status()
+        rc = self._lib.fabm_plan_set_host_output(self._h, nat.dptr(states), nat.dptr(f_cache), ctypes_ref(st))
+        if rc != nat.FABM_OK:
+            _raise_status(st)
+
+    def run_to_host(self, timeout_s: float = DEFAULT_TIMEOUT_S) -> Trajectory:
+        """Run with the trajectory streamed to fresh pinned host arrays during the
+        kernel (no D2H afterwards); falls back to run() + download() if pinned
+        memory is unavailable."""
+        N, d = int(self.grid.n_steps), int(self.problem.dim)
+        states = _PINNED.array(N + 1, d)
+        f_cache = _PINNED.array(N + 1, d) if states is not None else None
+        if f_cache is None:
+            self.run(timeout_s)
+            return self.download()
+        self.set_host_output(states, f_cache)
+        try:
+            self.run(timeout_s)
+        finally:
+            self.set_host_output(None, None)
+        grid = self.grid if isinstance(self.grid, GridSpec) else GridSpec(self.grid.n_steps, self.grid.h)
+        return Trajectory(grid=grid, states=states, f_cache=f_cache)
+
     def download(self) -> Trajectory:
         N, d = int(self.grid.n_steps), int(self.problem.dim)
         states = np.empty((N + 1, d))
@@ -231,6 +256,49 @@ class GpuPlan:
             self.close()
         except Exception:
             pass
+
+
+class _PinnedPool:
+    """Mapped pinned host buffers that the engine streams a trajectory into
+    during the run (``fabm_plan_set_host_output``), so ``solve_gpu`` needs no
+    D2H copy after the kernel.  Each solve takes fresh buffers; a buffer
+    returns to the pool when every array viewing it has been garbage
+    collected, so a returned ``Trajectory`` owns its memory as in the
+    reference (serial.py:55-56)."""
+
+    def __init__(self, keep_bytes: int = 1 << 31):
+        self.keep_bytes = keep_bytes
+        self.free: dict[int, list[int]] = {}
+        self.kept = 0
+
+    def take(self, nbytes: int) -> int | None:
+        lst = self.free.get(nbytes)
+        if lst:
+            self.kept -= nbytes
+            return lst.pop()
+        ptr = nat.load().fabm_host_alloc(nbytes)
+        return int(ptr) if ptr else None
+
+    def give(self, nbytes: int, ptr: int):
+        if self.kept + nbytes <= self.keep_bytes:
+            self.free.setdefault(nbytes, []).append(ptr)
+            self.kept += nbytes
+        else:
+            nat.load().fabm_host_free(ptr)
+
+    def array(self, rows: int, cols: int) -> np.ndarray | None:
+        import weakref
+
+        nbytes = 8 * rows * cols
+        ptr = self.take(nbytes)
+        if ptr is None:
+            return None
+        buf = (ctypes.c_double * (rows * cols)).from_address(ptr)
+        weakref.finalize(buf, self.give, nbytes, ptr)
+        return np.ctypeslib.as_array(buf).reshape(rows, cols)
+
+
+_PINNED = _PinnedPool()
 
 
 def ctypes_ref(obj):
@@ -289,8 +357,7 @@ def solve_gpu(
         # regenerate it on reuse (device modes cost ~1 ms at N=1e6)
         plan.set_weights(weights)
     plan.set_y0(problem.y0)
-    plan.run(timeout_s)
-    traj = plan.download()
+    traj = plan.run_to_host(timeout_s)
     if stats is not None:
         stats.update(plan.stats())
         stats["strategy"] = STRATEGY_NAME

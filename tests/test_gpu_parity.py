@@ -275,3 +275,33 @@ def test_watchdog_raises_strategy_timeout(fabm, monkeypatch):
     traj = fabm.solve_gpu(problem, grid, weights="reference")
     ref_states, _ = abm_oracle.solve_serial(problem.alpha, problem.y0, problem.rhs, grid.h, grid.n_steps)
     assert normwise_dev(traj.states, ref_states) <= 1e-12
+
+
+def test_streamed_host_output_equals_download(fabm):
+    # solve_gpu streams the trajectory into pinned host memory during the run;
+    # it must equal the device-resident result copied back afterwards
+    import gc
+
+    from paper_1611_08678_b200 import solver
+
+    problem = fabm.FractionalProblem(alpha=0.95, dim=3, rhs=fabm.rhs_chen(), y0=(-9.0, -5.0, 14.0), t_end=2.0)
+    grid = problem.grid(20000)
+    plan = fabm.GpuPlan(problem, grid)
+    plan.set_y0(problem.y0)
+    a = plan.run_to_host()
+    plan.run()
+    b = plan.download()
+    plan.close()
+    assert np.array_equal(a.states, b.states) and np.array_equal(a.f_cache, b.f_cache)
+    assert not a.states.flags.writeable
+    # buffers return to the pool when the trajectory dies, and are reused
+    nbytes = 8 * 3 * (grid.n_steps + 1)
+    solver._PINNED.keep_bytes = max(solver._PINNED.keep_bytes, solver._PINNED.kept + 2 * nbytes)
+    free = solver._PINNED.free.setdefault(nbytes, [])
+    n0 = len(free)
+    del a
+    gc.collect()
+    assert len(free) == n0 + 2
+    c = fabm.solve_gpu(problem, grid)
+    assert len(free) == n0
+    assert np.array_equal(c.states, b.states)
