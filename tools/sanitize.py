@@ -1,4 +1,4 @@
-"""Small invocations of every device entry point, for compute-sanitizer:
+"""Small invocations of every device entry point (a driver for compute-sanitizer where it is available;
   compute-sanitizer --tool memcheck  python tools/sanitize.py
   compute-sanitizer --tool synccheck python tools/sanitize.py
 (race detection / sanitizers on small N)."""

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "dfma_tile.cuh"
 
 using namespace fabm;
 

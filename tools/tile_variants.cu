@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "dfma_tile.cuh"
 
 using namespace fabm;
 
