@@ -3,20 +3,25 @@
 //
 // The reference integrates each problem with solve_serial (serial.py:114-176);
 // a sweep is a loop of such calls.  Here one persistent kernel (one CTA per
-// SM, 16 warps) integrates the whole sweep.  Work is cut into UNITS
-// (trajectory t, block J of 128 steps); a warp takes units from a global
-// ticket counter in the order u -> (t = u mod T, J = u div T), so all
-// trajectories advance together and the last wave is evenly filled.  A unit:
-//   1. pulls the bulk of its 128 targets from every completed block I < J:
-//      J Toeplitz chunks on the FP64 tensor cores (bulk_dmma.cuh, the same
-//      sweep as the single-trajectory agents) in ascending I — a fixed order,
-//      independent of which warp runs the unit, so results are bitwise
-//      deterministic;
-//   2. steps through the block: all 32 lanes run the sequential chain
-//      (serial.py:150-170) redundantly; lane l holds the sums of steps
-//      JB+4l..JB+4l+3 and pushes every new f_k into them (in-block window).
-// A unit waits (acquire) until unit (t, J-1) released the block J-1 rows;
-// that unit holds an earlier ticket, so its warp is already running.
+// SM, 16 warps) integrates the whole sweep.  Work is cut into tickets taken
+// from one global counter, in ROUNDS J = 0 .. nb-1 (block J = steps
+// 128J .. 128J+127 of every trajectory):
+//   * PULL units (t, J, s), s < S_J = ceil(J / G): the bulk of block J's 128
+//     targets from source blocks [sG, min(sG+G, J)) -- Toeplitz chunks on the
+//     FP64 tensor cores (bulk_dmma.cuh) in ascending order -- into a partial
+//     slot part[t][s];
+//   * STEP units (t, J): the partials summed in slot order s = 0, 1, ..., then
+//     the 128 steps of the block: all 32 lanes run the sequential chain
+//     (serial.py:150-170) redundantly; lane l holds the sums of steps
+//     JB+4l..JB+4l+3 and pushes every new f_k into them (in-block window).
+// Within a round all pulls (s-major) precede all steps.  A pull waits for
+// step (t, J-1) (previous round: an earlier ticket, so its warp is running);
+// a step waits for its round's pulls (earlier tickets too): no deadlock.
+// Splitting the pull over S_J warps keeps each trajectory's critical path
+// short (<= G chunks + 128 steps per round), so a few hundred trajectories
+// per GPU -- the 8-GPU share of the config 4 sweep -- still fill the machine.
+// The segment bounds depend only on J, so a trajectory's result is bitwise
+// independent of its batch neighbours and of the launch.
 #pragma once
 #include "engine.cuh"
 
@@ -43,10 +48,62 @@ struct BatchParams {
   unsigned long long* ticket;
   unsigned long long timeout_ns;
   DevCtrl* ctrl;
+  int G;                    // pull segment length (source blocks)
+  int S_max;                // pull segments of the largest round
+  const long long* round_start;  // [nb + 1]: first ticket of round J
+  double* part;             // [T][S_max][B * 2 * DS]: partial bulk sums (DMMA lane-major layout)
+  int* pulls_done;          // [T]: completed pull units (cumulative over rounds)
 };
 
+// pull units of round J: S_J = ceil(J / G), segment s = sources [sG, min(sG + G, J))
+__device__ __forceinline__ int pull_units(int J, int G) { return (J + G - 1) / G; }
+// pull units of rounds 0..J of one trajectory: sum_{j <= J} ceil(j / G)
+__device__ __forceinline__ long long pulls_through(int J, int G) {
+  const long long q = J / G, r = J % G;
+  return G * q * (q + 1) / 2 + (q + 1) * r;
+}
+
+template <int D>
+__device__ __forceinline__ double* part_slot(const BatchParams& P, int t, int s) {
+  return P.part + (static_cast<long long>(t) * P.S_max + s) * kB * 2 * Stride<D>::value;
+}
+
+// pull unit: sources [sG, min(sG + G, J)) into the targets of block J
+template <int D>
+__device__ void batch_pull(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int s, int lane) {
+  constexpr int DS = Stride<D>::value;
+  const double* wb = P.W + static_cast<long long>(t) * 3 * P.WL;
+  const double* wa = wb + P.WL;
+  const double* F = P.F + static_cast<long long>(t) * (P.nb + 1) * kB * DS;
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
+  const int i1 = min((s + 1) * P.G, J);
+  for (int I = s * P.G; I < i1; ++I) dmma_chunk<D>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
+  dmma_spill<D>(part_slot<D>(P, t, s), 0, lane, acc);
+}
+
+// spin until *flag >= want (acquire); false on abort or watchdog expiry
+__device__ __forceinline__ bool batch_wait(const BatchParams& P, const int* flag, long long want, int lane) {
+  int v = 0;
+  const unsigned long long w0 = global_ns();
+  for (;;) {
+    if (lane == 0) v = ld_acquire_gpu(flag);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v >= want) break;
+    if (*((volatile int*)&P.ctrl->abort)) return false;
+    if (global_ns() - w0 > P.timeout_ns) {
+      if (lane == 0) ctrl_abort(P.ctrl, ERR_TIMEOUT, KIND_NONE, -1, 0.0);
+      return false;
+    }
+    __nanosleep(200);
+  }
+  __syncwarp();
+  return true;
+}
+
+// step unit (t, J); false if the run was aborted while waiting for the pulls
 template <int SYS, int D>
-__device__ void batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int lane) {
+__device__ bool batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int lane) {
   constexpr int DS = Stride<D>::value;
   const long long N = P.N;
   const double* wb = P.W + static_cast<long long>(t) * 3 * P.WL;
@@ -65,13 +122,29 @@ __device__ void batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
   const double ha = P.ha[t], ig = P.ig[t];
   const long long JB = static_cast<long long>(J) * kB;
 
-  // ---- 1. bulk of sources I < J (ascending), then re-dealt through shared
-  // memory from the DMMA layout to the stepping layout (lane l: steps 4l..4l+3)
+  // ---- 1. the bulk of sources I < J: the round's partials summed in slot
+  // order (each an ascending DMMA chain), re-dealt through shared memory from
+  // the DMMA layout to the stepping layout (lane l: steps 4l..4l+3)
   double accP[kR][D], accC[kR][D];
   {
+    // total = ((p_0 + p_1) + ...) + p_{S_J - 1} over the round's pull units
     DmmaAcc<D> acc;
     dmma_zero<D>(acc);
-    for (int I = 0; I < J; ++I) dmma_chunk<D>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
+    const int np = pull_units(J, P.G);
+    if (!batch_wait(P, &P.pulls_done[t], pulls_through(J, P.G), lane)) return false;
+    if (np > 0) dmma_reload<D>(part_slot<D>(P, t, 0), 0, lane, acc);
+    for (int sg = 1; sg < np; ++sg) {
+      DmmaAcc<D> pa;
+      dmma_reload<D>(part_slot<D>(P, t, sg), 0, lane, pa);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+#pragma unroll
+          for (int w = 0; w < 2; ++w)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[h][c][w][e] = add_rn(acc[h][c][w][e], pa[h][c][w][e]);
+    }
     __syncwarp();
     double* rows = &A.f[0][0];  // [B][2][D]
 #pragma unroll
@@ -112,7 +185,7 @@ __device__ void batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
     }
     if (any_nonfinite<D>(f0)) {
       if (lane == 0) { P.err_kind[t] = KIND_INITIAL; P.err_step[t] = 0; }
-      return;
+      return true;
     }
   } else {
 #pragma unroll
@@ -215,6 +288,7 @@ __device__ void batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
     P.err_kind[t] = ekind;
     P.err_step[t] = estep;
   }
+  return true;
 }
 
 template <int SYS, int D>
@@ -222,35 +296,40 @@ __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   DmmaSmem<D>& A = reinterpret_cast<DmmaSmem<D>*>(smem_raw)[warp];
-  const unsigned long long total = static_cast<unsigned long long>(P.T) * P.nb;
+  const unsigned long long total = static_cast<unsigned long long>(P.round_start[P.nb]);
   for (;;) {
     unsigned long long u = 0;
     if (lane == 0) u = atomicAdd(P.ticket, 1ull);
     u = __shfl_sync(0xffffffffu, u, 0);
     if (u >= total) break;
-    const int t = static_cast<int>(u % P.T), J = static_cast<int>(u / P.T);
-    if (J > 0) {
-      // unit (t, J-1) holds an earlier ticket: its warp is running
-      int done = 0;
-      const unsigned long long w0 = global_ns();
-      for (;;) {
-        if (lane == 0) done = ld_acquire_gpu(&P.next_block[t]);
-        done = __shfl_sync(0xffffffffu, done, 0);
-        if (done >= J) break;
-        if (*((volatile int*)&P.ctrl->abort)) return;
-        if (global_ns() - w0 > P.timeout_ns) {
-          if (lane == 0) ctrl_abort(P.ctrl, ERR_TIMEOUT, KIND_NONE, -1, 0.0);
-          return;
-        }
-        __nanosleep(200);
-      }
-      __syncwarp();
+    // round J: the last J with round_start[J] <= u
+    int lo = 0, hi = P.nb - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (static_cast<unsigned long long>(__ldg(P.round_start + mid)) <= u) lo = mid; else hi = mid - 1;
     }
-    const bool dead = *((volatile int*)&P.err_kind[t]) != KIND_NONE;
-    if (!dead) batch_unit<SYS, D>(P, A, t, J, lane);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release_gpu(&P.next_block[t], J + 1);
+    const int J = lo;
+    const int SJ = pull_units(J, P.G);
+    const long long idx = static_cast<long long>(u) - __ldg(P.round_start + J);
+    if (idx < static_cast<long long>(P.T) * SJ) {  // ---- pull unit (t, J, s)
+      const int s = static_cast<int>(idx / P.T), t = static_cast<int>(idx % P.T);
+      if (!batch_wait(P, &P.next_block[t], J, lane)) return;
+      if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) batch_pull<D>(P, A, t, J, s, lane);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(&P.pulls_done[t], 1);
+    } else {  // ---- step unit (t, J)
+      const int t = static_cast<int>(idx - static_cast<long long>(P.T) * SJ);
+      if (!batch_wait(P, &P.next_block[t], J, lane)) return;
+      if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) {
+        if (!batch_unit<SYS, D>(P, A, t, J, lane)) return;
+      } else if (!batch_wait(P, &P.pulls_done[t], pulls_through(J, P.G), lane)) {
+        return;  // a dead trajectory's pulls still finish before the slots are reused
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(&P.next_block[t], J + 1);
+    }
   }
 }
 

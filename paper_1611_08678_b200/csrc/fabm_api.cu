@@ -778,7 +778,13 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
     for (int c = 0; c < D; ++c) hy0[static_cast<size_t>(t) * kMaxDim + c] = problems[t].y0[c];
     for (int i = 0; i < kMaxParams; ++i) hprm[static_cast<size_t>(t) * kMaxParams + i] = problems[t].params[i];
   }
-  DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl;
+  // pull segments: G source blocks per pull unit (batch.cuh); the ticket
+  // layout of round J is T * S_J pulls then T steps, S_J = ceil(J / G)
+  constexpr int kPullG = 32;
+  const int S_max = std::max(1, (nb - 1 + kPullG - 1) / kPullG);
+  std::vector<long long> hround(nb + 1, 0);
+  for (int J = 0; J < nb; ++J) hround[J + 1] = hround[J] + static_cast<long long>(T) * ((J + kPullG - 1) / kPullG + 1);
+  DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl, dround, dpart, dpdone;
   const size_t szF = sizeof(double) * static_cast<size_t>(T) * (nb + 1) * kB * DS;
   const size_t szY = sizeof(double) * static_cast<size_t>(T) * (N + 1) * D;
   CUDA_TRY(cudaMalloc(&dal.p, sizeof(double) * T));
@@ -798,6 +804,9 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   CUDA_TRY(cudaMalloc(&des.p, sizeof(long long) * T));
   CUDA_TRY(cudaMalloc(&dtk.p, sizeof(unsigned long long)));
   CUDA_TRY(cudaMalloc(&dctrl.p, sizeof(DevCtrl)));
+  CUDA_TRY(cudaMalloc(&dround.p, sizeof(long long) * (nb + 1)));
+  CUDA_TRY(cudaMalloc(&dpart.p, sizeof(double) * static_cast<size_t>(T) * S_max * kB * 2 * DS));
+  CUDA_TRY(cudaMalloc(&dpdone.p, sizeof(int) * T));
   cudaStream_t stream;
   CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   cudaEvent_t e0, e1;
@@ -821,6 +830,8 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   cudaMemsetAsync(des.p, 0, sizeof(long long) * T, stream);
   cudaMemsetAsync(dtk.p, 0, sizeof(unsigned long long), stream);
   cudaMemsetAsync(dctrl.p, 0, sizeof(DevCtrl), stream);
+  cudaMemsetAsync(dpdone.p, 0, sizeof(int) * T, stream);
+  cudaMemcpyAsync(dround.p, hround.data(), sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, stream);
   {
     const long long total = static_cast<long long>(T) * WL;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 64));
@@ -848,6 +859,11 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   P.ticket = dtk.as<unsigned long long>();
   P.timeout_ns = 600ull * 1000000000ull;
   P.ctrl = dctrl.as<DevCtrl>();
+  P.G = kPullG;
+  P.S_max = S_max;
+  P.round_start = dround.as<long long>();
+  P.part = dpart.as<double>();
+  P.pulls_done = dpdone.as<int>();
   cudaEventRecord(e0, stream);
   cudaError_t le = launch(P, prop.multiProcessorCount, stream);
   cudaEventRecord(e1, stream);
