@@ -267,24 +267,29 @@ class _PinnedPool:
     reference (serial.py:55-56)."""
 
     def __init__(self, keep_bytes: int = 1 << 31):
+        import threading
+
         self.keep_bytes = keep_bytes
         self.free: dict[int, list[int]] = {}
         self.kept = 0
+        self.lock = threading.Lock()
 
     def take(self, nbytes: int) -> int | None:
-        lst = self.free.get(nbytes)
-        if lst:
-            self.kept -= nbytes
-            return lst.pop()
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                self.kept -= nbytes
+                return lst.pop()
         ptr = nat.load().fabm_host_alloc(nbytes)
         return int(ptr) if ptr else None
 
     def give(self, nbytes: int, ptr: int):
-        if self.kept + nbytes <= self.keep_bytes:
-            self.free.setdefault(nbytes, []).append(ptr)
-            self.kept += nbytes
-        else:
-            nat.load().fabm_host_free(ptr)
+        with self.lock:
+            if self.kept + nbytes <= self.keep_bytes:
+                self.free.setdefault(nbytes, []).append(ptr)
+                self.kept += nbytes
+                return
+        nat.load().fabm_host_free(ptr)
 
     def array(self, rows: int, cols: int) -> np.ndarray | None:
         import weakref
@@ -294,7 +299,7 @@ class _PinnedPool:
         if ptr is None:
             return None
         buf = (ctypes.c_double * (rows * cols)).from_address(ptr)
-        weakref.finalize(buf, self.give, nbytes, ptr)
+        weakref.finalize(buf, self.give, nbytes, ptr).atexit = False  # process exit releases pinned memory
         return np.ctypeslib.as_array(buf).reshape(rows, cols)
 
 

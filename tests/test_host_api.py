@@ -244,3 +244,31 @@ class TestStrategyPlugin:
         # other strategies still reach the reference implementations
         traj = bench._solve_once(problem, "serial", 16, 1, 1024)
         assert traj.states.shape == (17, 1)
+
+
+class TestPinnedPool:
+    """Host logic of the pinned output pool (solver._PinnedPool) with a fake allocator."""
+
+    def test_reuse_and_cap(self, monkeypatch):
+        from paper_1611_08678_b200 import solver
+
+        allocs, frees = [], []
+
+        class FakeLib:
+            def fabm_host_alloc(self, n):
+                allocs.append(n)
+                return 0x1000 * len(allocs)
+
+            def fabm_host_free(self, p):
+                frees.append(p)
+
+        monkeypatch.setattr(solver.nat, "load", lambda: FakeLib())
+        pool = solver._PinnedPool(keep_bytes=100)
+        a = pool.take(64)
+        b = pool.take(64)
+        assert allocs == [64, 64] and a != b
+        pool.give(64, a)
+        assert pool.kept == 64 and pool.take(64) == a and pool.kept == 0
+        pool.give(64, a)
+        pool.give(64, b)  # over the cap: released, not kept
+        assert frees == [b] and pool.kept == 64
