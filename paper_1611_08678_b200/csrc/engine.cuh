@@ -134,7 +134,7 @@ __device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int
 struct StepperSmem {
   double wb[kSlots + 2 * kGFar];   // b_j, a_j for j < kSlots (zero beyond)
   double wa[kSlots + 2 * kGFar];
-  double ring[kRing][8];    // published step k: y_k at [0, d), f_k at [d, 2d)
+  double ring[kRing][12];   // published step k: y_k at [0, d), f_k at [d, 2d), fP of step k-1 at [2d, 3d)
   double hbuf[kHR][8];      // far handoff of step m: P part at [0, d), C part at [d, 2d)
   double xfer[2][8];        // near pre-sum of the next step, owner lane -> leader warp
   double tb[4 * kChunk];    // near weights, tb[j + 2*kChunk - 1] = b_j for j >= 1, 0 for j <= 0
@@ -225,8 +225,6 @@ struct LeaderState {
   // next chunk (B): lane l owns steps 32c + l
   double accA[2 * D], accB[2 * D];
   int cA;                // chunk index of A
-  int err_kind;
-  long long err_step;
 };
 
 // near sums of step m1 (owner lane -> all lanes via smem) and its far handoff.
@@ -311,17 +309,17 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   Rhs<SYS, D>::eval(t1, v, v + D, P.params);
   // publish (y_{n+1}, f_{n+1})
   const int ri = m1 & (kRing - 1);
-  if (lane == 0) st_pairs<D>(&S.ring[ri][0], v);
+  if (lane == 0) {
+    st_pairs<D>(&S.ring[ri][0], v);
+#pragma unroll
+    for (int c = 0; c < D; ++c) S.ring[ri][2 * D + c] = fP[c];  // checked by the writer warp
+  }
   mbar_arrive_if_u32(bars_u32 + 8u * static_cast<uint32_t>(ri), lane == 0);  // predicated: warp stays converged
   leader_push<D>(st, pw, v + D);
 #pragma unroll
   for (int c = 0; c < D; ++c) st.fc[c] = v[D + c];
-  // first non-finite rhs output: predictor before corrector (serial.py:157,167)
-  const bool bp = any_nonfinite<D>(fP), bc = any_nonfinite<D>(v + D);
-  const int kind = bp ? KIND_PREDICTOR : (bc ? KIND_CORRECTOR : KIND_NONE);
-  const bool first = (kind != KIND_NONE) & (st.err_kind == KIND_NONE);
-  st.err_kind = first ? kind : st.err_kind;
-  st.err_step = first ? n : st.err_step;
+  // non-finite rhs outputs are detected by the writer warp on the published
+  // rows (fP and f of every step), off the chain's SMSP
   // slow path: the far handoff of step n+1 was not ready when read
   if (!FAST && m1 < P.N && fl != m1) {
     if (!leader_wait_handoff(P, S, m1, waited)) return false;
@@ -360,13 +358,7 @@ template <int D>
 __device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
                                                    long long n_next, int lane, unsigned long long& throttled,
                                                    unsigned long long& lag_sum) {
-  if (st.err_kind != KIND_NONE) {
-    if (lane == 0)
-      raise_abort(P, ERR_NONFINITE, st.err_kind, st.err_step, static_cast<double>(st.err_step + 1) * P.h);
-    st_volatile_smem(&S.abort, 1);
-    if (lane == 0) mbar_arrive(&S.bars[n_next % kNumBars]);
-    return false;
-  }
+  if (ld_volatile_smem(&S.abort)) return false;  // the writer found a non-finite rhs output (or a watchdog fired)
   // ring back-pressure: the writer warp and every helper warp must have
   // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
   const long long lag = n_next - slowest_consumer(S);
@@ -410,8 +402,6 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) 
   if (bad0) return;
 
   const double b0 = P.wb[0], a0 = P.wa[0];
-  st.err_kind = KIND_NONE;
-  st.err_step = -1;
   unsigned long long waited = 0, throttled = 0;
   st.cA = 0;
 #pragma unroll
@@ -673,6 +663,26 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
       }
     }
     const long long k = k0 + lane;
+    // rows k >= 1 carry step n = k - 1: its predictor rhs fP and corrector rhs
+    // f_k; the first failing step, predictor before corrector (serial.py:157,167)
+    int kind = KIND_NONE;
+    if (k <= kend && k >= 1) {
+      const double* row = &S.ring[static_cast<int>(k % kRing)][0];
+      double fp[D], fk[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) { fp[c] = row[2 * D + c]; fk[c] = row[D + c]; }
+      kind = any_nonfinite<D>(fp) ? KIND_PREDICTOR : (any_nonfinite<D>(fk) ? KIND_CORRECTOR : KIND_NONE);
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, kind != KIND_NONE);
+    if (bad) {
+      const int first = __ffs(bad) - 1;
+      if (lane == first) {
+        const long long n = k - 1;
+        raise_abort(P, ERR_NONFINITE, kind, n, static_cast<double>(n + 1) * P.h);
+        st_volatile_smem(&S.abort, 1);
+      }
+      return;
+    }
     if (k <= kend) {
       const int ri = static_cast<int>(k % kRing);
       double yf[2 * D];
