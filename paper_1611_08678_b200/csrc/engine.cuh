@@ -37,7 +37,7 @@ constexpr int kBatch = 8;               // publishes consumed per helper wake-up
 constexpr int kThreads = 512;           // 16 warps per CTA (1 CTA per SM)
 constexpr int kWarps = kThreads / 32;
 constexpr int kRing = 64;               // published (y, f) ring in smem
-constexpr int kNumBars = 64;            // publish mbarriers (step k -> bar k % 64)
+constexpr int kNumBars = 64;            // publish mbarriers (step group g -> bar g % 64)
 constexpr int kHR = 128;                // far handoff ring (handoffs run ~60 steps ahead)
 constexpr int kR = 4;                   // rows per lane in 128-row warp loops (batch stepping)
 constexpr int kMaxOwn = 256;            // owned target blocks per agent
@@ -149,6 +149,13 @@ struct StepperSmem {
   int io_block;             // complete source blocks written by the writer warp
   int abort;
 };
+
+// publication groups: row 0 alone, then rows 8q-7 .. 8q+... : group of row k
+// is 0 for k = 0 and k/8 + 1 otherwise; a group's mbarrier completes when its
+// last row (k = 7 mod 8) or row N is published.  Consumers only wait for
+// rows that end a group (helper batches end at 7 mod 8 or N, writer batches
+// at 31 mod 32 or N), and each group completes its barrier exactly once.
+__device__ __forceinline__ int pub_group(long long k) { return k == 0 ? 0 : static_cast<int>(k >> 3) + 1; }
 
 __device__ __forceinline__ int helper_index(int warp) { return warp - (warp >> 2) - 1; }
 
@@ -314,7 +321,10 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
 #pragma unroll
     for (int c = 0; c < D; ++c) S.ring[ri][2 * D + c] = fP[c];  // checked by the writer warp
   }
-  mbar_arrive_if_u32(bars_u32 + 8u * static_cast<uint32_t>(ri), lane == 0);  // predicated: warp stays converged
+  // one release arrive per 8-step group (its last row, or row N), predicated:
+  // the warp stays converged and 7 of 8 steps carry no fence
+  const bool group_end = ((m1 & 7) == 7) | (m1 == static_cast<int>(P.N));
+  mbar_arrive_if_u32(bars_u32 + 8u * static_cast<uint32_t>(pub_group(m1) & (kNumBars - 1)), (lane == 0) & group_end);
   leader_push<D>(st, pw, v + D);
 #pragma unroll
   for (int c = 0; c < D; ++c) st.fc[c] = v[D + c];
@@ -572,8 +582,8 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
   // batches [0], [1, 7], [8, 15], [16, 23], ...: step 0 alone, since the
   // handoffs of chunks 0 and 1 need only f_0 and the leader waits for them
   for (int k0 = 0, kl = 0; k0 <= N; k0 = kl + 1, kl = (((k0 | (kBatch - 1)) < N) ? (k0 | (kBatch - 1)) : N)) {
-    uint64_t* bar = &S.bars[kl % kNumBars];
-    const uint32_t par = static_cast<uint32_t>((kl / kNumBars) & 1);
+    uint64_t* bar = &S.bars[pub_group(kl) % kNumBars];
+    const uint32_t par = static_cast<uint32_t>((pub_group(kl) / kNumBars) & 1);
     const long long c_w = clock64();
     if (!mbar_test(bar, par)) {
       unsigned spins = 0;
@@ -647,8 +657,8 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
   long long k0 = 0;
   while (k0 <= N) {
     const long long kend = (k0 + 31 < N) ? k0 + 31 : N;
-    uint64_t* bar = &S.bars[kend % kNumBars];
-    const uint32_t par = static_cast<uint32_t>((kend / kNumBars) & 1);
+    uint64_t* bar = &S.bars[pub_group(kend) % kNumBars];
+    const uint32_t par = static_cast<uint32_t>((pub_group(kend) / kNumBars) & 1);
     unsigned spins = 0;
     const unsigned long long w0 = global_ns();
     while (!mbar_wait_hint(bar, par, 100000u)) {

@@ -62,6 +62,13 @@ __global__ void chain(Prm p, long long steps, double* out, long long* cyc) {
       asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(
                        (unsigned)__cvta_generic_to_shared(&bar[(n + 1) & 63])) : "memory");
     if (V == 7) *(volatile int*)&flagw = (int)(n + 1);
+    if (V == 10 || V == 11) {  // ring store every step; 11: release arrive once per 8 steps
+      const int ri = (n + 1) & 63;
+      for (int c = 0; c < 3; ++c) { ring[ri][c] = y1[c]; ring[ri][4 + c] = f1[c]; }
+      if (V == 11 && ((n + 1) & 7) == 7)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&bar[((n + 1) >> 3) & 63])) : "memory");
+    }
     if (V >= 3 && V <= 4) {
       const int ri = (n + 1) & 63;
       for (int c = 0; c < 3; ++c) { ring[ri][c] = y1[c]; ring[ri][4 + c] = f1[c]; }
@@ -76,7 +83,7 @@ __global__ void chain(Prm p, long long steps, double* out, long long* cyc) {
     }
   }
   long long t1c = clock64();
-  out[0] = fc[0] + fc[1] + fc[2] + preP[0] + preC[1] + ((V >= 3 && V <= 8 && V != 5) ? ring[5][1] : 0.0) + flagw;
+  out[0] = fc[0] + fc[1] + fc[2] + preP[0] + preC[1] + ((V >= 3 && V <= 11 && V != 5 && V != 9) ? ring[5][1] : 0.0) + flagw;
   cyc[V] = t1c - t0;
 }
 
@@ -94,9 +101,11 @@ int main() {
   chain<7><<<1, 32>>>(p, steps, out, cyc);
   chain<8><<<1, 32>>>(p, steps, out, cyc);
   chain<9><<<1, 32>>>(p, steps, out, cyc);
+  chain<10><<<1, 32>>>(p, steps, out, cyc);
+  chain<11><<<1, 32>>>(p, steps, out, cyc);
   long long h[16];
   cudaMemcpy(h, cyc, 16 * 8, cudaMemcpyDeviceToHost);
-  for (int v = 1; v <= 9; ++v) printf("variant %d: %.1f cycles/step\n", v, h[v] / (double)steps);
+  for (int v = 1; v <= 11; ++v) printf("variant %d: %.1f cycles/step\n", v, h[v] / (double)steps);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
