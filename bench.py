@@ -297,13 +297,13 @@ def run_fabm(args, world, rank, local):
     d2h = 2 * (n + 1) * 3 * 8  # states + f_cache
     # warm the plan cache and the pinned output pool: a loop `traj = solve_gpu(...)`
     # holds the previous trajectory while the next one streams in (two buffer sets)
-    warm = [fabm.solve_gpu(problem, grid) for _ in range(2)]
+    warm = [fabm.solve_gpu(problem, grid, device=local) for _ in range(2)]
     del warm
     barrier(world)
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        traj = fabm.solve_gpu(problem, grid)
+        traj = fabm.solve_gpu(problem, grid, device=local)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t1)
     e2e_s = max_over_ranks(world, float(np.mean(times)))
@@ -480,7 +480,7 @@ def run_sharded(args, world, rank, local):
     plan.close()
     # e2e through the public collective call (host buffers, whole trajectory D2H on rank 0)
     t1 = time.perf_counter()
-    traj = parallel.solve_sharded(prob, grid) if world > 1 else fabm.solve_gpu(prob, grid)
+    traj = parallel.solve_sharded(prob, grid, device=local) if world > 1 else fabm.solve_gpu(prob, grid, device=local)
     e2e_s = max_over_ranks(world, time.perf_counter() - t1)
     if rank != 0:
         return
@@ -553,11 +553,11 @@ def run_csv(args, world, rank, local):
     value = world * rows / (step_ms * 1e-3)
     # e2e: the reference-facing call with host arrays, file included
     path2 = os.path.join(tmp, f"traj_e2e_{rank}.csv")
-    fabm.write_trajectory_csv(path2, traj)
+    fabm.write_trajectory_csv(path2, traj, device=local)
     times = []
     for _ in range(max(1, min(args.steps, 3))):
         t1 = time.perf_counter()
-        fabm.write_trajectory_csv(path2, traj)
+        fabm.write_trajectory_csv(path2, traj, device=local)
         times.append(time.perf_counter() - t1)
     e2e_s = max_over_ranks(world, float(np.mean(times)))
     data = Path(path2).read_bytes()
