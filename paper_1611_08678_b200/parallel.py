@@ -18,6 +18,8 @@ Two sharded paths:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 __all__ = ["shard_bounds", "gather_rows", "solve_batch_distributed", "solve_sharded"]
@@ -68,6 +70,8 @@ def solve_batch_distributed(problems, grid, *, solver=None, device: int | None =
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_bounds(len(problems), world, rank)
     kwargs = {"states": False}
+    if device is None and "LOCAL_RANK" in os.environ:
+        device = int(os.environ["LOCAL_RANK"])  # one process per GPU (torchrun)
     if device is not None:
         kwargs["device"] = device
     res = solver(problems[lo:hi], grid, **kwargs)
