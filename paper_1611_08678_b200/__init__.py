@@ -32,7 +32,7 @@ from .systems import (
     rhs_power_law,
     rhs_rossler,
 )
-from .output import format_trajectory_csv, write_trajectory_csv
+from .output import format_trajectory_csv, write_trajectory_csv, write_trajectory_npz
 from .solver import BatchResult, GpuPlan, device_count, measure_dfma_peak, solve_batch_gpu, solve_gpu
 
 __version__ = "0.1.0"
@@ -57,6 +57,7 @@ __all__ = [
     "measure_dfma_peak",
     "write_trajectory_csv",
     "format_trajectory_csv",
+    "write_trajectory_npz",
     "HindmarshRoseParams",
     "HR_DEFAULT_Y0",
     "SYSTEM_NAMES",

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native as nat
 
-__all__ = ["write_trajectory_csv", "format_trajectory_csv", "csv_upper_bound"]
+__all__ = ["write_trajectory_csv", "format_trajectory_csv", "write_trajectory_npz", "csv_upper_bound"]
 
 FIELD_MAX = 24  # "-1.2345678901234567e-308"
 
@@ -127,3 +127,14 @@ def plan_write_csv(plan, path, *, stats: dict | None = None) -> None:
         _raise(st, p)
     if stats is not None:
         stats.update(kernel_ms=ms.value, bytes=n.value)
+
+
+def write_trajectory_npz(path, traj) -> None:
+    """Binary companion of the CSV: ``t``, ``states`` and
+    ``f_cache`` (when present) as float64 arrays in one uncompressed .npz --
+    exact, ~3x smaller than the 17-digit text and written at disk speed."""
+    arrays = {"t": np.asarray(traj.t, dtype=np.float64), "states": np.asarray(traj.states, dtype=np.float64)}
+    f_cache = getattr(traj, "f_cache", None)
+    if f_cache is not None:
+        arrays["f_cache"] = np.asarray(f_cache, dtype=np.float64)
+    np.savez(_check_path(path), **arrays)

@@ -272,3 +272,16 @@ class TestPinnedPool:
         pool.give(64, a)
         pool.give(64, b)  # over the cap: released, not kept
         assert frees == [b] and pool.kept == 64
+
+
+def test_write_trajectory_npz_round_trip(tmp_path):
+    import paper_1611_08678_b200 as fabm
+
+    grid = fabm.GridSpec(n_steps=4, h=0.25)
+    states = np.arange(15, dtype=np.float64).reshape(5, 3) / 7.0
+    traj = fabm.Trajectory(grid=grid, states=states, f_cache=-states)
+    path = tmp_path / "t.npz"
+    fabm.write_trajectory_npz(path, traj)
+    with np.load(path) as z:
+        assert np.array_equal(z["t"], grid.times())
+        assert np.array_equal(z["states"], states) and np.array_equal(z["f_cache"], -states)
