@@ -38,3 +38,6 @@ late = rows[:, 3] - rows[:, 4]
 print("late blocks (staged after need):", int(np.nansum(late > 0)), "total late us:", float(np.nansum(np.clip(late, 0, None))))
 for J, src, rdy, stg, need in rows[::max(1, k // 20)]:
     print(f"J={int(J):6d} src@{src:9.1f} ready@{rdy:9.1f} staged@{stg:9.1f} need@{need:9.1f}")
+# where the stepper loses time: lateness per decile of the run
+dec = np.array_split(np.arange(k), 10)
+print("late us per decile of target blocks:", [round(float(np.nansum(np.clip(late[d], 0, None))) / 1e3, 2) for d in dec], "ms")
