@@ -33,6 +33,7 @@ from .systems import (
     rhs_rossler,
 )
 from .output import format_trajectory_csv, write_trajectory_csv, write_trajectory_npz
+from .strategies import make_partition, solve_block_parallel, solve_reduction_parallel
 from .solver import BatchResult, GpuPlan, device_count, measure_dfma_peak, solve_batch_gpu, solve_gpu
 
 __version__ = "0.1.0"
@@ -51,6 +52,9 @@ __all__ = [
     "precompute_weights",
     "solve_gpu",
     "solve_batch_gpu",
+    "solve_block_parallel",
+    "solve_reduction_parallel",
+    "make_partition",
     "BatchResult",
     "GpuPlan",
     "device_count",

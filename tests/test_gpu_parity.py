@@ -305,3 +305,19 @@ def test_streamed_host_output_equals_download(fabm):
     c = fabm.solve_gpu(problem, grid)
     assert len(free) == n0
     assert np.array_equal(c.states, b.states)
+
+
+def test_parallel_strategy_entry_points(fabm):
+    # fodeabm.solve_block_parallel / solve_reduction_parallel names on the engine:
+    # equivalent to solve_serial (reference EQUIV_TOL 1e-10; here the 1e-12 contract)
+    g = golden("hindmarsh_rose")
+    problem, grid = problem_from_golden(g)
+    st_b, st_r = {}, {}
+    blk = fabm.solve_block_parallel(problem, grid, 4, stats=st_b)
+    red = fabm.solve_reduction_parallel(problem, grid, 3, 256, stats=st_r)
+    ref = g["states"]
+    rows = g["rows"]
+    assert normwise_dev(blk.states[rows], ref) <= 1e-12 and normwise_dev(red.states[rows], ref) <= 1e-12
+    assert np.array_equal(blk.states, fabm.solve_gpu(problem, grid, weights="reference").states)
+    assert st_b["plan"].n_workers == 4 and len(st_b["idle_steps"]) == 4 and st_r["chunk"] == 256
+    assert st_b["kernel_ms"] > 0

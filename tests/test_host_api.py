@@ -285,3 +285,29 @@ def test_write_trajectory_npz_round_trip(tmp_path):
     with np.load(path) as z:
         assert np.array_equal(z["t"], grid.times())
         assert np.array_equal(z["states"], states) and np.array_equal(z["f_cache"], -states)
+
+
+class TestParallelStrategyEntryPoints:
+    """solve_block_parallel / solve_reduction_parallel keep the reference's
+    validation (partition.py:54-74, reduction.py:158-164) before any device work."""
+
+    def test_partition_matches_reference_rules(self):
+        plan = fabm.make_partition(10, 3)
+        assert plan.block_size == 4 and plan.blocks == ((0, 4), (4, 8), (8, 10))
+        for n, p in [(0, 1), (5, 0), (3, 4)]:
+            with pytest.raises(ValueError):
+                fabm.make_partition(n, p)
+
+    def test_bad_arguments_raise_value_error(self):
+        problem = fabm.FractionalProblem(alpha=0.5, dim=1, rhs=fabm.rhs_linear(-1.0), y0=[1.0], t_end=1.0)
+        grid = problem.grid(16)
+        with pytest.raises(ValueError):
+            fabm.solve_block_parallel(problem, grid, 0)
+        with pytest.raises(ValueError):
+            fabm.solve_block_parallel(problem, grid, 17)
+        with pytest.raises(ValueError):
+            fabm.solve_reduction_parallel(problem, grid, 2, chunk=0)
+        with pytest.raises(ValueError):
+            fabm.solve_reduction_parallel(problem, grid, 0)
+        with pytest.raises(ValueError):
+            fabm.solve_block_parallel(problem, fabm.GridSpec(n_steps=16, h=0.5), 2)
