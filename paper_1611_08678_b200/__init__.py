@@ -33,7 +33,16 @@ from .systems import (
     rhs_rossler,
 )
 from .output import format_trajectory_csv, write_trajectory_csv, write_trajectory_npz
-from .strategies import make_partition, solve_block_parallel, solve_reduction_parallel
+from .steps import step_corrector, step_predictor
+from .strategies import (
+    PartitionPlan,
+    idle_fraction,
+    make_partition,
+    owner,
+    solve_block_parallel,
+    solve_reduction_parallel,
+)
+from .verify import ConvergenceReport, exact_power_law, mittag_leffler, observed_order
 from .solver import BatchResult, GpuPlan, device_count, measure_dfma_peak, solve_batch_gpu, solve_gpu
 
 __version__ = "0.1.0"
@@ -55,6 +64,15 @@ __all__ = [
     "solve_block_parallel",
     "solve_reduction_parallel",
     "make_partition",
+    "PartitionPlan",
+    "owner",
+    "idle_fraction",
+    "step_predictor",
+    "step_corrector",
+    "ConvergenceReport",
+    "mittag_leffler",
+    "exact_power_law",
+    "observed_order",
     "BatchResult",
     "GpuPlan",
     "device_count",

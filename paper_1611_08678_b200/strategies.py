@@ -23,7 +23,8 @@ import numpy as np
 
 from .solver import solve_gpu
 
-__all__ = ["PartitionPlan", "make_partition", "solve_block_parallel", "solve_reduction_parallel"]
+__all__ = ["PartitionPlan", "make_partition", "owner", "idle_fraction", "solve_block_parallel",
+           "solve_reduction_parallel"]
 
 DEFAULT_WATCHDOG_S = 60.0  # parallel/_shm.py:35
 
@@ -51,6 +52,20 @@ def make_partition(n_steps: int, n_workers: int) -> PartitionPlan:
     block = -(-n_steps // n_workers)
     blocks = tuple((min(p * block, n_steps), min((p + 1) * block, n_steps)) for p in range(n_workers))
     return PartitionPlan(n_steps=n_steps, n_workers=n_workers, block_size=block, blocks=blocks)
+
+
+def owner(plan: PartitionPlan, n: int) -> int:
+    """Index of the worker whose block contains step n (partition.py:76-80)."""
+    if not 0 <= n < plan.n_steps:
+        raise IndexError(f"step index {n} outside [0, {plan.n_steps})")
+    return min(n // plan.block_size, plan.n_workers - 1)
+
+
+def idle_fraction(plan: PartitionPlan, worker: int) -> float:
+    """Fraction of steps before the iteration reaches a worker's block (partition.py:83-93)."""
+    if not 0 <= worker < plan.n_workers:
+        raise IndexError(f"worker index {worker} outside [0, {plan.n_workers})")
+    return min(worker * plan.block_size, plan.n_steps) / plan.n_steps
 
 
 def _check_grid(problem, grid):

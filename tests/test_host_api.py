@@ -311,3 +311,23 @@ class TestParallelStrategyEntryPoints:
             fabm.solve_reduction_parallel(problem, grid, 0)
         with pytest.raises(ValueError):
             fabm.solve_block_parallel(problem, fabm.GridSpec(n_steps=16, h=0.5), 2)
+
+
+def test_partition_helpers_match_reference_rules():
+    plan = fabm.make_partition(10, 3)
+    assert [fabm.owner(plan, n) for n in range(10)] == [0, 0, 0, 0, 1, 1, 1, 1, 2, 2]
+    assert [fabm.idle_fraction(plan, w) for w in range(3)] == [0.0, 0.4, 0.8]
+    with pytest.raises(IndexError):
+        fabm.owner(plan, 10)
+
+
+def test_public_names_cover_the_reference_api():
+    # every name fodeabm exports (fodeabm/__init__.py:41-71) except the CPU
+    # solver itself, which solve_gpu replaces
+    ref_all = ["FractionalProblem", "GridSpec", "WeightTable", "Trajectory", "PartitionPlan", "ConvergenceReport",
+               "HindmarshRoseParams", "SolverStepError", "StrategyTimeoutError", "gamma", "predictor_weight",
+               "corrector_weight_a", "corrector_weight_c", "precompute_weights", "step_predictor", "step_corrector",
+               "make_partition", "owner", "idle_fraction", "solve_block_parallel", "solve_reduction_parallel",
+               "rhs_constant", "rhs_power_law", "rhs_linear", "rhs_hindmarsh_rose", "mittag_leffler",
+               "exact_power_law", "observed_order"]
+    assert [n for n in ref_all if not hasattr(fabm, n)] == []
