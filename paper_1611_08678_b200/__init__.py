@@ -43,7 +43,15 @@ from .strategies import (
     solve_reduction_parallel,
 )
 from .verify import ConvergenceReport, exact_power_law, mittag_leffler, observed_order
-from .solver import BatchResult, GpuPlan, device_count, measure_dfma_peak, solve_batch_gpu, solve_gpu
+from .solver import (
+    BatchResult,
+    GpuPlan,
+    device_count,
+    measure_dfma_peak,
+    release_cached_memory,
+    solve_batch_gpu,
+    solve_gpu,
+)
 
 __version__ = "0.1.0"
 
@@ -77,6 +85,7 @@ __all__ = [
     "GpuPlan",
     "device_count",
     "measure_dfma_peak",
+    "release_cached_memory",
     "write_trajectory_csv",
     "format_trajectory_csv",
     "write_trajectory_npz",

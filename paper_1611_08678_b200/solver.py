@@ -30,7 +30,7 @@ from .core import GridSpec, SolverStepError, StrategyTimeoutError, Trajectory, p
 from .systems import device_system_of
 
 __all__ = ["solve_gpu", "solve_batch_gpu", "BatchResult", "GpuPlan", "device_count", "measure_dfma_peak",
-           "STRATEGY_NAME"]
+           "release_cached_memory", "STRATEGY_NAME"]
 
 STRATEGY_NAME = "gpu"
 # the reference watchdog default (_shm.py:35); FABM_TIMEOUT_S overrides it
@@ -331,6 +331,20 @@ def _cached_plan(problem, grid, weights, device) -> GpuPlan:
         while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
             _PLAN_CACHE.popitem(last=False)[1].close()
     return plan
+
+
+def release_cached_memory() -> None:
+    """Free what solve_gpu keeps between calls: the cached plans (device
+    buffers of the last problem sizes) and the pooled pinned output buffers
+    (trajectories still alive keep theirs)."""
+    while _PLAN_CACHE:
+        _PLAN_CACHE.popitem(last=False)[1].close()
+    with _PINNED.lock:
+        free, _PINNED.free, _PINNED.kept = _PINNED.free, {}, 0
+    lib = nat.load()
+    for ptrs in free.values():
+        for ptr in ptrs:
+            lib.fabm_host_free(ptr)
 
 
 def solve_gpu(

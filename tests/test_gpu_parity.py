@@ -321,3 +321,14 @@ def test_parallel_strategy_entry_points(fabm):
     assert np.array_equal(blk.states, fabm.solve_gpu(problem, grid, weights="reference").states)
     assert st_b["plan"].n_workers == 4 and len(st_b["idle_steps"]) == 4 and st_r["chunk"] == 256
     assert st_b["kernel_ms"] > 0
+
+
+def test_release_cached_memory(fabm):
+    from paper_1611_08678_b200 import solver
+
+    problem = fabm.FractionalProblem(alpha=0.8, dim=1, rhs=fabm.rhs_linear(-1.0), y0=[1.0], t_end=1.0)
+    a = fabm.solve_gpu(problem, problem.grid(3000))
+    fabm.release_cached_memory()
+    assert not solver._PLAN_CACHE and solver._PINNED.kept == 0
+    b = fabm.solve_gpu(problem, problem.grid(3000))  # plans and buffers come back on demand
+    assert np.array_equal(a.states, b.states)
