@@ -97,6 +97,65 @@ __device__ __forceinline__ void dmma_chunk(const double* __restrict__ wbp, const
   }
 }
 
+// ---- pipelined variant (two staging buffers): the staging of chunk I+1 is
+// issued as asynchronous copies (LDGSTS) and lands while chunk I is swept;
+// src_bytes = 0 zero-fills.  Everything staged is final when read (read-only
+// weights, f rows of completed source blocks), so .ca copies are safe.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int D>
+__device__ __forceinline__ void dmma_stage_async(const double* __restrict__ wbp, const double* __restrict__ wap,
+                                                 const double* Fp, DmmaSmem<D>& S, int T0, int X, int xend,
+                                                 int lane) {
+  constexpr int DS = Stride<D>::value;
+  const long long wbase = static_cast<long long>(T0) - X - 127;
+  for (int u = lane; u < 256; u += 32) {
+    cp_async8(&S.w[0][u], wbp + wbase + u, 8);
+    cp_async8(&S.w[1][u], wap + wbase + u, 8);
+  }
+  for (int rho = lane; rho < kDRows; rho += 32) {
+    const int row = X - 56 + rho;
+    const bool ok = row >= 0 && row < xend;
+    const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+    for (int c = 0; c < D; ++c) cp_async8(&S.f[c][dmma_fidx(rho)], src + c, ok ? 8 : 0);
+  }
+  cp_async_commit();
+}
+
+// the sweep of an already staged chunk (the DMMA sequence of dmma_chunk)
+template <int D>
+__device__ __forceinline__ void dmma_sweep(const DmmaSmem<D>& S, int X, int xend, int lane, DmmaAcc<D>& acc) {
+  const int i = lane >> 2, k = lane & 3;
+  const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
+#pragma unroll 2
+  for (int v = 0; v < nsteps; ++v) {
+    const int sbr = 4 * v;
+    double a[2][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = 64 * h + i - k + 183 - sbr;
+      a[h][0] = S.w[0][u];
+      a[h][1] = S.w[1][u];
+    }
+    const int rho = sbr + k + 8 * i;
+    double b[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+  }
+}
+
 template <int D>
 __device__ __forceinline__ void dmma_zero(DmmaAcc<D>& acc) {
 #pragma unroll
