@@ -267,6 +267,11 @@ int fabm_step_pc(const fabm_problem* problem, const fabm_grid* grid,
                  double* yp_out, double* y_out, int32_t* err_out, int device,
                  fabm_status* status);
 
+/* Return the device memory that batch solves keep cached in the device's
+ * stream-ordered pool (fabm_solve_batch allocates from it so repeated sweeps
+ * skip cudaMalloc/cudaFree). */
+int fabm_trim_memory(int device);
+
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
 /* measured FP64 FMA throughput (FMA/s) of a DFMA-bound loop on `device` */
 double fabm_measure_dfma_peak(int device);

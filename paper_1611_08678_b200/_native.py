@@ -65,6 +65,7 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_set_host_output",
     "fabm_host_alloc",
     "fabm_host_free",
+    "fabm_trim_memory",
 )
 
 
@@ -156,6 +157,7 @@ def _declare(lib):
         "fabm_plan_set_host_output": (ctypes.c_int, [plan, _DP, _DP, S]),
         "fabm_host_alloc": (ctypes.c_void_p, [ctypes.c_int64]),
         "fabm_host_free": (None, [ctypes.c_void_p]),
+        "fabm_trim_memory": (ctypes.c_int, [ctypes.c_int]),
         "fabm_step_pc": (ctypes.c_int, [P, G, _DP, _DP, _DP, ctypes.c_int64, _DP, ctypes.c_int64, _I64P,
                                         ctypes.c_int64, _DP, _DP, _DP, ctypes.POINTER(ctypes.c_int32), ctypes.c_int,
                                         S]),

@@ -717,14 +717,44 @@ BatchLaunch pick_batch(int sys, int dim) {
   FABM_PICK_SYSTEM(launch_batch);
 }
 
+// device buffer; with a stream it is stream-ordered (cudaMallocAsync from the
+// device's default pool, freed back to the pool without a device sync)
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t s = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (s) cudaFreeAsync(p, s);
+      else cudaFree(p);
+    }
+  }
+  cudaError_t alloc(size_t bytes, cudaStream_t stream) {
+    s = stream;
+    return cudaMallocAsync(&p, bytes, stream);
   }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
 };
+// the stream outlives the buffers declared after it (reverse destruction order)
+struct StreamHolder {
+  cudaStream_t s = nullptr;
+  ~StreamHolder() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+// keep freed pool memory cached on the device: repeated batch solves of the
+// same size then allocate without cudaMalloc/cudaFree (~100 ms per GB-scale
+// sweep otherwise)
+void retain_pool_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -790,38 +820,39 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   const int S_max = std::max(1, (nb - 1 + kPullG - 1) / kPullG);
   std::vector<long long> hround(nb + 1, 0);
   for (int J = 0; J < nb; ++J) hround[J + 1] = hround[J] + static_cast<long long>(T) * ((J + kPullG - 1) / kPullG + 1);
+  StreamHolder stream_holder;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream_holder.s, cudaStreamNonBlocking));
+  cudaStream_t stream = stream_holder.s;
+  retain_pool_memory(device);
   DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl, dround, dpart, dpdone;
   const size_t szF = sizeof(double) * static_cast<size_t>(T) * (nb + 1) * kB * DS;
   const size_t szY = sizeof(double) * static_cast<size_t>(T) * (N + 1) * D;
-  CUDA_TRY(cudaMalloc(&dal.p, sizeof(double) * T));
-  CUDA_TRY(cudaMalloc(&dg1.p, sizeof(double) * T));
-  CUDA_TRY(cudaMalloc(&dg2.p, sizeof(double) * T));
-  CUDA_TRY(cudaMalloc(&dha.p, sizeof(double) * T));
-  CUDA_TRY(cudaMalloc(&dig.p, sizeof(double) * T));
-  CUDA_TRY(cudaMalloc(&dy0.p, sizeof(double) * hy0.size()));
-  CUDA_TRY(cudaMalloc(&dprm.p, sizeof(double) * hprm.size()));
-  CUDA_TRY(cudaMalloc(&dW.p, sizeof(double) * static_cast<size_t>(T) * 3 * WL));
-  CUDA_TRY(cudaMalloc(&dF.p, szF));
-  if (states) CUDA_TRY(cudaMalloc(&dY.p, szY));
-  if (f_cache) CUDA_TRY(cudaMalloc(&dFc.p, szY));
-  CUDA_TRY(cudaMalloc(&dyl.p, sizeof(double) * static_cast<size_t>(T) * D));
-  CUDA_TRY(cudaMalloc(&dnext.p, sizeof(int) * T));
-  CUDA_TRY(cudaMalloc(&dek.p, sizeof(int) * T));
-  CUDA_TRY(cudaMalloc(&des.p, sizeof(long long) * T));
-  CUDA_TRY(cudaMalloc(&dtk.p, sizeof(unsigned long long)));
-  CUDA_TRY(cudaMalloc(&dctrl.p, sizeof(DevCtrl)));
-  CUDA_TRY(cudaMalloc(&dround.p, sizeof(long long) * (nb + 1)));
-  CUDA_TRY(cudaMalloc(&dpart.p, sizeof(double) * static_cast<size_t>(T) * S_max * kB * 2 * DS));
-  CUDA_TRY(cudaMalloc(&dpdone.p, sizeof(int) * T));
-  cudaStream_t stream;
-  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CUDA_TRY(dal.alloc(sizeof(double) * T, stream));
+  CUDA_TRY(dg1.alloc(sizeof(double) * T, stream));
+  CUDA_TRY(dg2.alloc(sizeof(double) * T, stream));
+  CUDA_TRY(dha.alloc(sizeof(double) * T, stream));
+  CUDA_TRY(dig.alloc(sizeof(double) * T, stream));
+  CUDA_TRY(dy0.alloc(sizeof(double) * hy0.size(), stream));
+  CUDA_TRY(dprm.alloc(sizeof(double) * hprm.size(), stream));
+  CUDA_TRY(dW.alloc(sizeof(double) * static_cast<size_t>(T) * 3 * WL, stream));
+  CUDA_TRY(dF.alloc(szF, stream));
+  if (states) CUDA_TRY(dY.alloc(szY, stream));
+  if (f_cache) CUDA_TRY(dFc.alloc(szY, stream));
+  CUDA_TRY(dyl.alloc(sizeof(double) * static_cast<size_t>(T) * D, stream));
+  CUDA_TRY(dnext.alloc(sizeof(int) * T, stream));
+  CUDA_TRY(dek.alloc(sizeof(int) * T, stream));
+  CUDA_TRY(des.alloc(sizeof(long long) * T, stream));
+  CUDA_TRY(dtk.alloc(sizeof(unsigned long long), stream));
+  CUDA_TRY(dctrl.alloc(sizeof(DevCtrl), stream));
+  CUDA_TRY(dround.alloc(sizeof(long long) * (nb + 1), stream));
+  CUDA_TRY(dpart.alloc(sizeof(double) * static_cast<size_t>(T) * S_max * kB * 2 * DS, stream));
+  CUDA_TRY(dpdone.alloc(sizeof(int) * T, stream));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   auto cleanup = [&]() {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaStreamDestroy(stream);
   };
   cudaMemcpyAsync(dal.p, hal.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
   cudaMemcpyAsync(dg1.p, hg1.data(), sizeof(double) * T, cudaMemcpyHostToDevice, stream);
@@ -1375,3 +1406,11 @@ int fabm_plan_set_host_output(fabm_plan* p, double* states, double* f_cache, fab
 }
 
 }  // extern "C"
+
+extern "C" int fabm_trim_memory(int device) {
+  cudaMemPool_t pool;
+  if (cudaSetDevice(device) != cudaSuccess) return FABM_ERR_NODEVICE;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return FABM_ERR_CUDA;
+  cudaDeviceSynchronize();
+  return cudaMemPoolTrimTo(pool, 0) == cudaSuccess ? FABM_OK : FABM_ERR_CUDA;
+}

@@ -333,10 +333,11 @@ def _cached_plan(problem, grid, weights, device) -> GpuPlan:
     return plan
 
 
-def release_cached_memory() -> None:
-    """Free what solve_gpu keeps between calls: the cached plans (device
-    buffers of the last problem sizes) and the pooled pinned output buffers
-    (trajectories still alive keep theirs)."""
+def release_cached_memory(device: int | None = None) -> None:
+    """Free what the solvers keep between calls: the cached plans (device
+    buffers of the last problem sizes), the pooled pinned output buffers
+    (trajectories still alive keep theirs) and the device memory pool the
+    batch solver allocates from (on ``device``, default: every device)."""
     while _PLAN_CACHE:
         _PLAN_CACHE.popitem(last=False)[1].close()
     with _PINNED.lock:
@@ -345,6 +346,8 @@ def release_cached_memory() -> None:
     for ptrs in free.values():
         for ptr in ptrs:
             lib.fabm_host_free(ptr)
+    for dev in ([device] if device is not None else range(int(lib.fabm_device_count()))):
+        lib.fabm_trim_memory(int(dev))
 
 
 def solve_gpu(
