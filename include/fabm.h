@@ -163,7 +163,8 @@ void fabm_plan_destroy(fabm_plan* plan);
 
 /* Stream the next runs' trajectory (states, f_cache: (n_steps+1)*dim doubles
  * each) straight into pinned host memory while the kernel runs, so no D2H
- * copy follows the solve.  The buffers must be mapped pinned memory, e.g.
+ * copy follows the solve (how solve_gpu returns the Trajectory of
+ * serial.py:36-64 as fresh host arrays; no reference counterpart).  The buffers must be mapped pinned memory, e.g.
  * from fabm_host_alloc, and stay valid until the plan is reset with NULLs or
  * destroyed.  Both NULL: back to device-only output (fabm_plan_download). */
 int fabm_plan_set_host_output(fabm_plan* plan, double* states, double* f_cache,
@@ -269,7 +270,8 @@ int fabm_step_pc(const fabm_problem* problem, const fabm_grid* grid,
 
 /* Return the device memory that batch solves keep cached in the device's
  * stream-ordered pool (fabm_solve_batch allocates from it so repeated sweeps
- * skip cudaMalloc/cudaFree). */
+ * skip cudaMalloc/cudaFree).  Resource management only; no reference
+ * counterpart. */
 int fabm_trim_memory(int device);
 
 /* ---- microbenchmarks used by bench.py for the roofline denominator ----- */
