@@ -298,12 +298,6 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   double nr[2 * D], fr[2 * D];
   const int fl = leader_gather<D, ROT>(S, st, m1, lane, nr, fr, !FAST);
   const PushW pw = leader_push_weights<false>(S, st.cA, m1, lane);
-  double nxP[D], nxC[D];  // pre-sums of step n+1 = near + far
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    nxP[c] = nr[c] + fr[c];
-    nxC[c] = nr[D + c] + fr[D + c];
-  }
   const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
   const double ha = P.ha;
   double yP[D], fP[D], v[2 * D];
@@ -334,16 +328,13 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   if (!FAST && m1 < P.N && fl != m1) {
     if (!leader_wait_handoff(P, S, m1, waited)) return false;
     ld_pairs<D>(&S.hbuf[m1 & (kHR - 1)][0], fr);
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      nxP[c] = nr[c] + fr[c];
-      nxC[c] = nr[D + c] + fr[D + c];
-    }
   }
+  // pre-sums of step n+1 = near + far, consumed after this step's chain so
+  // the shared-memory loads of the gather complete under it
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    st.preP[c] = nxP[c];
-    st.preC[c] = nxC[c];
+    st.preP[c] = nr[c] + fr[c];
+    st.preC[c] = nr[D + c] + fr[D + c];
   }
   return true;
 }
