@@ -83,3 +83,32 @@ def test_batch_mixed_members_rejected(fabm):
     b = fabm.FractionalProblem(alpha=0.8, dim=3, rhs=fabm.rhs_chen(), y0=(1, 1, 1), t_end=1.0)
     with pytest.raises(ValueError):
         fabm.solve_batch_gpu([a, b], a.grid(10))
+
+
+@pytest.mark.parametrize("kind", ["power-law", "constant4", "linear4", "hindmarsh-rose"])
+def test_batch_other_systems_and_dims(fabm, kind):
+    # every device rhs family through the batch engine (d = 1, 3, 4), vs the oracle
+    rng = np.random.default_rng(len(kind))
+    alphas = rng.uniform(0.3, 1.0, 5)
+    N = 700
+    probs = []
+    for a in alphas:
+        a = float(a)
+        if kind == "power-law":
+            probs.append(fabm.FractionalProblem(alpha=a, dim=1, rhs=fabm.rhs_power_law(a, 2.5), y0=[0.0], t_end=1.0))
+        elif kind == "constant4":
+            probs.append(fabm.FractionalProblem(alpha=a, dim=4, rhs=fabm.rhs_constant([1.0, -2.0, 0.5, 3.0]),
+                                                y0=[0.0, 1.0, 2.0, 3.0], t_end=1.0))
+        elif kind == "linear4":
+            probs.append(fabm.FractionalProblem(alpha=a, dim=4, rhs=fabm.rhs_linear(-0.9), y0=[1.0, -1.0, 0.5, 2.0],
+                                                t_end=1.0))
+        else:
+            probs.append(fabm.FractionalProblem(alpha=a, dim=3, rhs=fabm.rhs_hindmarsh_rose(), y0=fabm.HR_DEFAULT_Y0,
+                                                t_end=7.0))
+    grid = probs[0].grid(N)
+    res = fabm.solve_batch_gpu(probs, grid, f_cache=True)
+    for i, p in enumerate(probs):
+        w = abm_oracle.accurate_weights(p.alpha, N)
+        ref, fref = abm_oracle.solve_serial(p.alpha, p.y0, p.rhs, grid.h, N, weights=w)
+        assert normwise_dev(res.states[i], ref) <= TOL
+        assert normwise_dev(res.f_cache[i], fref) <= TOL
