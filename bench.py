@@ -420,6 +420,31 @@ def run_batch(args, world, rank, local):
         return
     peak_fma = fabm.measure_dfma_peak(local)
     fma = 3.0 * n * n * T
+    # CPU port of the reference on two members of the sweep (prefixes, all
+    # host threads), projected with t = a M + c M^2 to the whole sweep
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        from oracle import abm_oracle, c_oracle
+
+        c_oracle.build()
+        threads = c_oracle.max_threads()
+        samples = []
+        for m in (16000, 32000):
+            t0 = time.perf_counter()
+            for i in (0, T - 1):
+                p = probs[i]
+                tag = p.rhs.device_system
+                c_oracle.solve(tag.name, tag.params, p.alpha, p.y0, h, m,
+                               abm_oracle.reference_weights(p.alpha, m), threads=threads)
+            samples.append((m, (time.perf_counter() - t0) / 2))
+        (m1, t1), (m2, t2) = samples
+        c2 = (t2 / m2 - t1 / m1) / (m2 - m1)
+        a1 = max(t1 / m1 - c2 * m1, 0.0)
+        per_traj = a1 * n + c2 * n * n
+        cpu = {"value": n / per_traj, "unit": "steps/s", "cores": threads, "kind": "port",
+               "sample": (f"oracle/abm_oracle.c ({threads} OpenMP threads) on two sweep members, prefixes M={m1} "
+                          f"({t1:.2f}s) and M={m2} ({t2:.2f}s) each; projected {per_traj:.1f}s per trajectory, "
+                          f"{per_traj * T / 3600:.1f} h for the sweep")}
     achieved = 2.0 * fma / (step_ms * 1e-3) / 1e12 / world
     print(json.dumps({
         "metric": "ABM trajectory-steps/sec, financial alpha sweep (BASELINE config 4)",
@@ -431,6 +456,7 @@ def run_batch(args, world, rank, local):
         "history_fma_per_s": fma / (step_ms * 1e-3),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": 2.0 * peak_fma / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / (2.0 * peak_fma / 1e12), "traffic": None},
+        "cpu_baseline": cpu,
         "e2e": {"value": T * n / e2e_s, "unit": "steps/s",
                 "h2d_bytes_per_step": T * 8 * (16 + 4 + 5), "d2h_bytes_per_step": T * 3 * 8,
                 "note": "solve_batch_gpu wall time per sweep (host problems in, y_N out; max over ranks)"},
