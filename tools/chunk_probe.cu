@@ -30,6 +30,88 @@ __global__ void __launch_bounds__(kThreads, 1) chunk_kernel(const double* wb, co
   out[blockIdx.x * kThreads + threadIdx.x] = s;
 }
 
+// variant: the two weight windows staged by TMA bulk copies (one elected
+// lane, mbarrier completion), the f rows by the lanes as in dmma_chunk
+template <int D>
+struct alignas(128) TmaSmem {
+  double w[2][264];  // 258 used: the window starts one double early when misaligned
+  double f[D][kDPad];
+  uint64_t bar;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) tma_kernel(const double* wb, const double* wa, const double* F,
+                                                          int chunks, double* out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int DS = Stride<D>::value;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto& S = reinterpret_cast<TmaSmem<D>*>(smem_raw)[warp];
+  if (lane == 0) mbar_init(&S.bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
+  const int J = chunks + kL + (blockIdx.x * kWarps + warp) % 64;
+  const int T0 = J * kB, xend = (J - kL + 1) * kB;
+  uint32_t phase = 0;
+  for (int I = 0; I < chunks; ++I) {
+    const int X = I * kB;
+    __syncwarp();
+    const long long wbase = static_cast<long long>(T0) - X - 127;
+    const long long wal = wbase & ~1ll;
+    const int off = static_cast<int>(wbase - wal);
+    if (lane == 0) {
+      const uint32_t bar = smem_u32(&S.bar);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * 2064) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(&S.w[0][0])), "l"(wb + wal), "r"(2064), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(&S.w[1][0])), "l"(wa + wal), "r"(2064), "r"(bar) : "memory");
+    }
+    for (int rho = lane; rho < kDRows; rho += 32) {
+      const int row = X - 56 + rho;
+      const bool ok = row >= 0 && row < xend;
+      const double* src = F + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+      for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = ok ? __ldcg(src + c) : 0.0;
+    }
+    while (!mbar_try(&S.bar, phase)) {}
+    phase ^= 1;
+    __syncwarp();
+    const int i = lane >> 2, k = lane & 3;
+    const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
+#pragma unroll 2
+    for (int v = 0; v < nsteps; ++v) {
+      const int sbr = 4 * v;
+      double a[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 64 * h + i - k + 183 - sbr + off;
+        a[h][0] = S.w[0][u];
+        a[h][1] = S.w[1][u];
+      }
+      const int rho = sbr + k + 8 * i;
+      double b[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+#pragma unroll
+          for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) s += acc[h][c][w][0] + acc[h][c][w][1];
+  out[blockIdx.x * kThreads + threadIdx.x] = s;
+}
+
 int main() {
   constexpr int D = 3;
   const int chunks = 256, nsm = 148;
@@ -64,5 +146,27 @@ int main() {
   const double fma = (double)nsm * kWarps * chunks * 2.0 * kB * kB * D;
   printf("engine chunk (bulk_dmma.cuh): %.3f ms  %.4e FMA/s  (%s)\n", best, fma / (best * 1e-3),
          cudaGetErrorString(cudaGetLastError()));
+  std::vector<double> ref(nsm * kThreads), got(nsm * kThreads);
+  cudaMemcpy(ref.data(), out, 8 * ref.size(), cudaMemcpyDeviceToHost);
+  {
+    const size_t tsmem = kWarps * sizeof(TmaSmem<D>);
+    cudaFuncSetAttribute(tma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    tma_kernel<D><<<nsm, kThreads, tsmem>>>(wb, wa, F, 8, out);
+    float tb = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      tma_kernel<D><<<nsm, kThreads, tsmem>>>(wb, wa, F, chunks, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tb = ms < tb ? ms : tb;
+    }
+    cudaMemcpy(got.data(), out, 8 * got.size(), cudaMemcpyDeviceToHost);
+    bool same = true;
+    for (size_t q = 0; q < ref.size(); ++q) same &= ref[q] == got[q];
+    printf("TMA weights + lane f staging: %.3f ms  %.4e FMA/s  bitwise %s (%s)\n", tb, fma / (tb * 1e-3),
+           same ? "equal" : "DIFFERENT", cudaGetErrorString(cudaGetLastError()));
+  }
   return 0;
 }
