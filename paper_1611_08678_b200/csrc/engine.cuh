@@ -364,10 +364,10 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
   // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
   const long long lag = n_next - slowest_consumer(S);
   lag_sum += static_cast<unsigned long long>(lag);
-  if (lag > kRing - 24) {
+  if (lag > kRing - 32) {
     unsigned spins = 0;
     const unsigned long long w0 = global_ns();
-    while (n_next - slowest_consumer(S) > kRing - 24) {
+    while (n_next - slowest_consumer(S) > kRing - 32) {
       if (((++spins) & 1023u) == 0) {
         if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
         if (global_ns() - w0 > P.timeout_ns) {
@@ -454,7 +454,9 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) 
         if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n + u, lane, bars_u32, waited)) return;
     }
     n += 8;
-    if (!solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
+    // back-pressure / abort check every 16 steps (its 9 shared-memory loads
+    // stall the in-order issue); the lag bound leaves room for 16 more steps
+    if ((n & 15) == 0 && !solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   }
 #pragma unroll 1
   for (; n < N32; ++n)
