@@ -233,6 +233,7 @@ def run_reference(args, world, rank):
             times.append(info["projected_seconds"])
     t_full = statistics.median(times)
     value = n / t_full
+    extra = reference_python_sample(n)
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -252,7 +253,45 @@ def run_reference(args, world, rank):
         "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if extra is not None:
+        out["reference_python_serial"] = extra
     print(json.dumps(out))
+
+
+def reference_python_sample(n_target: int) -> dict | None:
+    """The unmodified reference (fodeabm.solve_serial, Python + NumPy, one core)
+    on two prefixes of the headline run, projected with its own O(N^2) model;
+    only when the reference is installed at baseline/_ref (it travels with the
+    repo snapshot).  Reported beside the C port, which is the faster baseline."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "fodeabm").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import fodeabm
+
+        sigma, rho, beta = 10.0, 28.0, 8.0 / 3.0
+
+        def lorenz(t, y):
+            return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
+
+        h = T_END / N_STEPS
+        samples = []
+        for m in (5000, 10000):
+            prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
+            t0 = time.perf_counter()
+            fodeabm.solve_serial(prob, fodeabm.GridSpec(n_steps=m, h=h))
+            samples.append((m, time.perf_counter() - t0))
+        (m1, t1), (m2, t2) = samples
+        c = (t2 / m2 - t1 / m1) / (m2 - m1)
+        a = max(t1 / m1 - c * m1, 0.0)
+        t_full = a * n_target + c * n_target * n_target
+        return {"value": n_target / t_full, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": (f"fodeabm.solve_serial (baseline/_ref, Python+NumPy) Lorenz prefixes M={m1} ({t1:.2f}s) "
+                           f"and M={m2} ({t2:.2f}s); projected t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}")}
+    except Exception as exc:  # noqa: BLE001 - informational only
+        return {"error": f"{type(exc).__name__}: {exc}"}
 
 
 def run_fabm(args, world, rank, local):
