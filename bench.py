@@ -278,7 +278,7 @@ def reference_python_sample(n_target: int) -> dict | None:
 
         h = T_END / N_STEPS
         samples = []
-        for m in (5000, 10000):
+        for m in (10000, 20000):
             prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
             t0 = time.perf_counter()
             fodeabm.solve_serial(prob, fodeabm.GridSpec(n_steps=m, h=h))
