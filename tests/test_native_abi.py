@@ -69,3 +69,32 @@ def test_config_errors_need_no_device(lib):
     rc = lib.fabm_weights(1.5, 3, 0, 0.0, 0.0, b, b, b, ctypes.byref(st))
     assert rc == _native.FABM_ERR_CONFIG
     assert b"alpha" in st.message
+
+
+def test_new_entry_points_validate_before_any_device_work(lib):
+    # argument errors are reported as FABM_ERR_CONFIG (the reference's
+    # ValueError) before any CUDA call, so they behave the same without a GPU
+    from paper_1611_08678_b200 import _native
+
+    st = _native.Status()
+    one = (ctypes.c_double * 4)(1.0, 2.0, 3.0, 4.0)
+    n = ctypes.c_int64(0)
+    # CSV: dim 0
+    rc = lib.fabm_format_csv(one, None, 1, 0, 0.1, 0, None, 0, ctypes.byref(n), None, ctypes.byref(st))
+    assert rc == _native.FABM_ERR_CONFIG
+    # Mittag-Leffler: negative count
+    rc = lib.fabm_mittag_leffler(one, one, -1, 0, one, None, ctypes.byref(st))
+    assert rc == _native.FABM_ERR_CONFIG
+    # step ops: index outside [0, N)
+    pr, gr = _native.Problem(), _native.Grid()
+    pr.alpha, pr.dim, pr.system = 0.5, 1, 2
+    pr.params[0] = -1.0
+    gr.n_steps, gr.h = 3, 0.1
+    ns = (ctypes.c_int64 * 1)(3)
+    err = (ctypes.c_int32 * 1)()
+    rc = lib.fabm_step_pc(ctypes.byref(pr), ctypes.byref(gr), one, one, one, 4, one, 4, ns, 1, None, one, one, err, 0,
+                          ctypes.byref(st))
+    assert rc == _native.FABM_ERR_CONFIG and b"outside" in st.message
+    # a null plan
+    assert lib.fabm_plan_set_host_output(None, None, None, ctypes.byref(st)) == _native.FABM_ERR_CONFIG
+    assert lib.fabm_plan_write_csv(None, b"x.csv", None, None, ctypes.byref(st)) == _native.FABM_ERR_CONFIG
