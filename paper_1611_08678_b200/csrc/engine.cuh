@@ -6,17 +6,21 @@
 //   yP = P_n*h^a + y0; fP = f(t,yP); y = (C_n + fP/G2)*h^a + y0; f_{n+1} = f(t,y)
 //
 // Work split:
-//   * CTA 0 is the STEPPER.  One leader thread runs the sequential chain of
-//     every step; 384 helper threads each own one future step ("slot") and
-//     push every newly published f_k into it (window k in [lo(m), m-G]);
-//     an I/O warp streams y/f to HBM, publishes completed source blocks and
-//     stages the bulk sums of the next target block into shared memory.
-//   * CTAs 1.. are BULK agents (one per warp).  Agent a owns target blocks
-//     J = L + a + i*A and accumulates the Toeplitz products T_{J-I} F_I of
-//     every completed source block I <= J-L, in ascending I (deterministic),
-//     earliest-deadline target first.  Tile = 128 targets x 128 sources,
-//     register-blocked 4 targets x d components x {b,a} per lane, weights
-//     staged in a mod-4 transposed smem layout (conflict-free sliding window).
+//   * CTA 0 is the STEPPER.  The leader warp (warp 0, alone on SMSP 0) runs
+//     the sequential chain of every step on all 32 lanes and keeps the near
+//     window (the last 32-64 steps) in registers; 8 helper warps own 512
+//     future steps ("slots") and push every published f_k of the far window
+//     into them, handing each step's far part to the leader ~30 steps ahead;
+//     the writer warp streams (y, f) to HBM (and pinned host memory) and
+//     checks every rhs output for non-finite values; the publisher warp
+//     releases completed source blocks to the bulk agents and stages each
+//     target block's bulk sums into shared memory.
+//   * CTAs 1.. are BULK agents (one per warp, 16 per SM).  Agent a owns target
+//     blocks J = L + a + i*A and accumulates the Toeplitz products T_{J-I} F_I
+//     of every completed source block I <= J-L, in ascending I (deterministic),
+//     earliest-deadline target first.  Tile = 128 targets x 128 sources on the
+//     FP64 tensor cores (bulk_dmma.cuh: m8n8k4 DMMA, 8 diagonal shifts of one
+//     weight fragment per instruction).
 // The only host interaction is the launch; there is no round trip per step.
 #pragma once
 #include "device_common.cuh"
