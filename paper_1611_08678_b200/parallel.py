@@ -22,7 +22,18 @@ import os
 
 import numpy as np
 
-__all__ = ["shard_bounds", "gather_rows", "solve_batch_distributed", "solve_sharded"]
+# the reference's fodeabm.parallel names (parallel/__init__.py), on the engine
+from .strategies import (  # noqa: E402,F401
+    PartitionPlan,
+    idle_fraction,
+    make_partition,
+    owner,
+    solve_block_parallel,
+    solve_reduction_parallel,
+)
+
+__all__ = ["shard_bounds", "gather_rows", "solve_batch_distributed", "solve_sharded", "PartitionPlan",
+           "make_partition", "owner", "idle_fraction", "solve_block_parallel", "solve_reduction_parallel"]
 
 
 def shard_bounds(count: int, world: int, rank: int) -> tuple[int, int]:

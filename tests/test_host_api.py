@@ -331,3 +331,19 @@ def test_public_names_cover_the_reference_api():
                "rhs_constant", "rhs_power_law", "rhs_linear", "rhs_hindmarsh_rose", "mittag_leffler",
                "exact_power_law", "observed_order"]
     assert [n for n in ref_all if not hasattr(fabm, n)] == []
+
+
+def test_reference_module_layout_is_mirrored():
+    # fodeabm.parallel / fodeabm.checks / fodeabm.verify / fodeabm.systems names
+    from paper_1611_08678_b200 import checks, parallel, systems, verify
+
+    for name in ("solve_block_parallel", "solve_reduction_parallel", "make_partition", "owner", "idle_fraction",
+                 "PartitionPlan"):
+        assert hasattr(parallel, name), name
+    for name in ("CheckResult", "check_power_law_orders", "check_constant_forcing", "check_linear_mittag_leffler",
+                 "check_strategy_equivalence", "run_verification_suite"):
+        assert hasattr(checks, name), name
+    for name in ("mittag_leffler", "exact_power_law", "observed_order", "ConvergenceReport"):
+        assert hasattr(verify, name), name
+    for name in ("rhs_constant", "rhs_power_law", "rhs_linear", "rhs_hindmarsh_rose", "HindmarshRoseParams"):
+        assert hasattr(systems, name), name
