@@ -95,3 +95,24 @@ def test_random_batch_vs_c_oracle(fabm, seed):
         w = abm_oracle.accurate_weights(p.alpha, N)
         ref, _ = _oracle(p, grid, w)
         assert normwise_dev(res.states[i], ref) <= TOL, (T, N, p.alpha)
+
+
+@pytest.mark.parametrize("seed", range(max(4, N_CASES // 10)))
+def test_random_virtual_shards_bitwise(fabm, seed):
+    # the sharded protocol (one-GPU emulation, K shards) is bitwise the single-GPU solve
+    rng = np.random.default_rng(3000 + seed)
+    kind, problem, grid = _case(fabm, rng)
+    K = int(rng.integers(2, 9))
+    try:
+        ref = fabm.solve_gpu(problem, grid)
+    except fabm.SolverStepError:
+        return
+    plan = fabm.GpuPlan(problem, grid)
+    try:
+        plan.set_virtual_shards(K)
+        plan.set_y0(problem.y0)
+        plan.run()
+        got = plan.download()
+    finally:
+        plan.close()
+    assert np.array_equal(got.states, ref.states), (kind, K, grid.n_steps)
