@@ -12,9 +12,10 @@ using namespace fabm;
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) chunk_kernel(const double* wb, const double* wa, const double* F,
-                                                            int chunks, double* out) {
+                                                            int chunks, double* out, int active = kWarps) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= active) return;
   auto* S = reinterpret_cast<DmmaSmem<D>*>(smem_raw) + warp;
   DmmaAcc<D> acc;
   dmma_zero<D>(acc);
@@ -146,6 +147,23 @@ int main() {
   const double fma = (double)nsm * kWarps * chunks * 2.0 * kB * kB * D;
   printf("engine chunk (bulk_dmma.cuh): %.3f ms  %.4e FMA/s  (%s)\n", best, fma / (best * 1e-3),
          cudaGetErrorString(cudaGetLastError()));
+  for (int active : {1, 2, 4, 8}) {  // lone-warp chunk rate (the per-chain cap of the schedule)
+    float tb = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0);
+      chunk_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out, active);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tb = ms < tb ? ms : tb;
+    }
+    const double f1 = (double)nsm * active * chunks * 2.0 * kB * kB * D;
+    printf("  %2d warp(s)/SM: %.4e FMA/s = %.3f of the 16-warp rate per SM\n", active, f1 / (tb * 1e-3),
+           (f1 / (tb * 1e-3)) / (fma / (best * 1e-3)));
+  }
+  chunk_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out);
+  cudaDeviceSynchronize();
   std::vector<double> ref(nsm * kThreads), got(nsm * kThreads);
   cudaMemcpy(ref.data(), out, 8 * ref.size(), cudaMemcpyDeviceToHost);
   {
