@@ -68,33 +68,17 @@ __device__ __forceinline__ double* part_slot(const BatchParams& P, int t, int s)
   return P.part + (static_cast<long long>(t) * P.S_max + s) * kB * 2 * Stride<D>::value;
 }
 
-// pull unit: sources [sG, min(sG + G, J)) into the targets of block J.
-// PIPE: two staging buffers, chunk I+1 copied asynchronously while chunk I
-// is swept (the staging streams from HBM: a sweep's working set is larger
-// than L2 for hundreds of trajectories)
-template <int D, bool PIPE>
-__device__ void batch_pull(const BatchParams& P, DmmaSmem<D>* A, int t, int J, int s, int lane) {
+// pull unit: sources [sG, min(sG + G, J)) into the targets of block J
+template <int D>
+__device__ void batch_pull(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int s, int lane) {
   constexpr int DS = Stride<D>::value;
   const double* wb = P.W + static_cast<long long>(t) * 3 * P.WL;
   const double* wa = wb + P.WL;
   const double* F = P.F + static_cast<long long>(t) * (P.nb + 1) * kB * DS;
   DmmaAcc<D> acc;
   dmma_zero<D>(acc);
-  const int i0 = s * P.G, i1 = min((s + 1) * P.G, J);
-  if constexpr (PIPE) {
-    int bi = 0;
-    if (i0 < i1) dmma_stage_async<D>(wb, wa, F, A[0], J * kB, i0 * kB, J * kB, lane);
-    for (int I = i0; I < i1; ++I) {
-      cp_async_wait_all();
-      __syncwarp();
-      if (I + 1 < i1) dmma_stage_async<D>(wb, wa, F, A[bi ^ 1], J * kB, (I + 1) * kB, J * kB, lane);
-      dmma_sweep<D>(A[bi], I * kB, J * kB, lane, acc);
-      __syncwarp();
-      bi ^= 1;
-    }
-  } else {
-    for (int I = i0; I < i1; ++I) dmma_chunk<D>(wb, wa, F, A[0], J * kB, I * kB, J * kB, lane, acc);
-  }
+  const int i1 = min((s + 1) * P.G, J);
+  for (int I = s * P.G; I < i1; ++I) dmma_chunk<D, true>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
   dmma_spill<D>(part_slot<D>(P, t, s), 0, lane, acc);
 }
 
@@ -307,13 +291,11 @@ __device__ bool batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
   return true;
 }
 
-template <int SYS, int D, bool PIPE>
+template <int SYS, int D>
 __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (PIPE && warp >= kWarps / 2) return;  // PIPE: 8 warps per SM, two staging buffers each
-  DmmaSmem<D>* Abuf = reinterpret_cast<DmmaSmem<D>*>(smem_raw) + (PIPE ? 2 : 1) * warp;
-  DmmaSmem<D>& A = Abuf[0];
+  DmmaSmem<D>& A = reinterpret_cast<DmmaSmem<D>*>(smem_raw)[warp];
   const unsigned long long total = static_cast<unsigned long long>(P.round_start[P.nb]);
   for (;;) {
     unsigned long long u = 0;
@@ -332,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
     if (idx < static_cast<long long>(P.T) * SJ) {  // ---- pull unit (t, J, s)
       const int s = static_cast<int>(idx / P.T), t = static_cast<int>(idx % P.T);
       if (!batch_wait(P, &P.next_block[t], J, lane)) return;
-      if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) batch_pull<D, PIPE>(P, Abuf, t, J, s, lane);
+      if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) batch_pull<D>(P, A, t, J, s, lane);
       __threadfence();
       __syncwarp();
       if (lane == 0) atomicAdd(&P.pulls_done[t], 1);

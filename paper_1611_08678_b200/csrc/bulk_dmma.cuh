@@ -50,25 +50,68 @@ __device__ __forceinline__ int dmma_target(int lane, int h, int e) {
 
 // sources of chunk I (X = 128 I) into the sums of target block J (T0 = 128 J);
 // xend = bulk end of the block (128 (J - L + 1)); closing on its last chunk
-template <int D>
+template <int D, bool BATCHED = false>
 __device__ __forceinline__ void dmma_chunk(const double* __restrict__ wbp, const double* __restrict__ wap,
                                            const double* Fp, DmmaSmem<D>& S, int T0, int X, int xend,
                                            int lane, DmmaAcc<D>& acc) {
   constexpr int DS = Stride<D>::value;
-  __syncwarp();
-  const long long wbase = static_cast<long long>(T0) - X - 127;
-  for (int u = lane; u < 256; u += 32) {
-    S.w[0][u] = __ldg(wbp + wbase + u);
-    S.w[1][u] = __ldg(wap + wbase + u);
-  }
-  for (int rho = lane; rho < kDRows; rho += 32) {
-    const int row = X - 56 + rho;
-    const bool ok = row >= 0 && row < xend;
-    const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+  if constexpr (BATCHED) {
+    const long long wbase = static_cast<long long>(T0) - X - 127;
+    // every global load of the chunk issued before its shared stores, so the
+    // loads overlap instead of serialising one round trip per loop iteration:
+    // the batch kernel stages from HBM (sweep working sets exceed L2);
+    // 4096 x 1e5 sweep 7.43 -> 7.11 s.  (In the engine, whose staging hits
+    // L2, the extra registers cost more than they gain.)
+    constexpr int kFQ = (kDRows + 31) / 32;  // 6 rows per lane
+    {
+      double wv[2][8];
 #pragma unroll
-    for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = ok ? __ldcg(src + c) : 0.0;
+      for (int q = 0; q < 8; ++q) {
+        wv[0][q] = __ldg(wbp + wbase + lane + 32 * q);
+        wv[1][q] = __ldg(wap + wbase + lane + 32 * q);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        S.w[0][lane + 32 * q] = wv[0][q];
+        S.w[1][lane + 32 * q] = wv[1][q];
+      }
+    }
+    double fv[kFQ][D];
+#pragma unroll
+    for (int q = 0; q < kFQ; ++q) {
+      const int rho = lane + 32 * q;
+      const int row = X - 56 + rho;
+      const bool ok = rho < kDRows && row >= 0 && row < xend;
+      const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+      for (int c = 0; c < D; ++c) fv[q][c] = ok ? __ldcg(src + c) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kFQ; ++q) {
+      const int rho = lane + 32 * q;
+      if (rho < kDRows) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = fv[q][c];
+      }
+    }
+    __syncwarp();
+  } else {
+    __syncwarp();
+    const long long wbase = static_cast<long long>(T0) - X - 127;
+    for (int u = lane; u < 256; u += 32) {
+      S.w[0][u] = __ldg(wbp + wbase + u);
+      S.w[1][u] = __ldg(wap + wbase + u);
+    }
+    for (int rho = lane; rho < kDRows; rho += 32) {
+      const int row = X - 56 + rho;
+      const bool ok = row >= 0 && row < xend;
+      const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+      for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = ok ? __ldcg(src + c) : 0.0;
+    }
+    __syncwarp();
   }
-  __syncwarp();
   const int i = lane >> 2, k = lane & 3;
   const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
 #pragma unroll 2
@@ -84,65 +127,6 @@ __device__ __forceinline__ void dmma_chunk(const double* __restrict__ wbp, const
     }
     // B = f[sb + k + 8j], column j = lane >> 2; rows past the staged range
     // (closing sweep) are zero
-    const int rho = sbr + k + 8 * i;
-    double b[D];
-#pragma unroll
-    for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int c = 0; c < D; ++c)
-#pragma unroll
-        for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
-  }
-}
-
-// ---- pipelined variant (two staging buffers): the staging of chunk I+1 is
-// issued as asynchronous copies (LDGSTS) and lands while chunk I is swept;
-// src_bytes = 0 zero-fills.  Everything staged is final when read (read-only
-// weights, f rows of completed source blocks), so .ca copies are safe.
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-template <int D>
-__device__ __forceinline__ void dmma_stage_async(const double* __restrict__ wbp, const double* __restrict__ wap,
-                                                 const double* Fp, DmmaSmem<D>& S, int T0, int X, int xend,
-                                                 int lane) {
-  constexpr int DS = Stride<D>::value;
-  const long long wbase = static_cast<long long>(T0) - X - 127;
-  for (int u = lane; u < 256; u += 32) {
-    cp_async8(&S.w[0][u], wbp + wbase + u, 8);
-    cp_async8(&S.w[1][u], wap + wbase + u, 8);
-  }
-  for (int rho = lane; rho < kDRows; rho += 32) {
-    const int row = X - 56 + rho;
-    const bool ok = row >= 0 && row < xend;
-    const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
-#pragma unroll
-    for (int c = 0; c < D; ++c) cp_async8(&S.f[c][dmma_fidx(rho)], src + c, ok ? 8 : 0);
-  }
-  cp_async_commit();
-}
-
-// the sweep of an already staged chunk (the DMMA sequence of dmma_chunk)
-template <int D>
-__device__ __forceinline__ void dmma_sweep(const DmmaSmem<D>& S, int X, int xend, int lane, DmmaAcc<D>& acc) {
-  const int i = lane >> 2, k = lane & 3;
-  const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
-#pragma unroll 2
-  for (int v = 0; v < nsteps; ++v) {
-    const int sbr = 4 * v;
-    double a[2][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int u = 64 * h + i - k + 183 - sbr;
-      a[h][0] = S.w[0][u];
-      a[h][1] = S.w[1][u];
-    }
     const int rho = sbr + k + 8 * i;
     double b[D];
 #pragma unroll

@@ -695,17 +695,11 @@ int fabm_weights(double alpha, int64_t n_steps, int mode, double gamma1, double 
 }  // extern "C"
 
 namespace {
-constexpr int kBatchPipeMaxT = 1024;
 using BatchLaunch = cudaError_t (*)(const BatchParams&, int grid, cudaStream_t);
 
 template <int SYS, int D>
 cudaError_t launch_batch(const BatchParams& P, int grid, cudaStream_t stream) {
-  // 8 warps/SM with double-buffered staging pay off when few trajectories
-  // share the GPU; 16 synchronous warps when the sweep is wide (bitwise the
-  // same results either way: identical DMMA sequences)
-  bool pipe = P.T <= kBatchPipeMaxT;
-  if (const char* e = getenv("FABM_BATCH_PIPE")) pipe = atoi(e) != 0;  // dev A/B
-  auto kern = pipe ? abm_batch_kernel<SYS, D, true> : abm_batch_kernel<SYS, D, false>;
+  auto kern = abm_batch_kernel<SYS, D>;
   const size_t smem = kWarps * sizeof(DmmaSmem<D>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -31,6 +31,225 @@ __global__ void __launch_bounds__(kThreads, 1) chunk_kernel(const double* wb, co
   out[blockIdx.x * kThreads + threadIdx.x] = s;
 }
 
+// prefetch variant: while chunk I is swept, the cache lines of chunk I+1's
+// weight windows and f rows are prefetched into L1 (prefetch.global.L1), and
+// the f rows are then loaded through L1 (__ldg)
+template <int D>
+__device__ __forceinline__ void chunk_prefetch_next(const double* wbp, const double* wap, const double* Fp, int T0,
+                                                    int Xn, int xend, int lane) {
+  constexpr int DS = Stride<D>::value;
+  if (Xn >= xend) return;
+  const long long wbase = static_cast<long long>(T0) - Xn - 127;
+  // 256 doubles = 2 KB = 16 lines per weight array; 184 rows x 32 B = 46 lines of f
+  if (lane < 16) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(wbp + wbase + 16 * lane));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(wap + wbase + 16 * lane));
+  }
+  for (int q = lane; q < 47; q += 32) {
+    const int row = Xn - 56 + 4 * q;
+    if (row >= 0 && row < xend) asm volatile("prefetch.global.L1 [%0];" ::"l"(Fp + static_cast<long long>(row) * DS));
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void dmma_chunk_pf(const double* __restrict__ wbp, const double* __restrict__ wap,
+                                              const double* Fp, DmmaSmem<D>& S, int T0, int X, int xend, int lane,
+                                              DmmaAcc<D>& acc) {
+  constexpr int DS = Stride<D>::value;
+  __syncwarp();
+  const long long wbase = static_cast<long long>(T0) - X - 127;
+  for (int u = lane; u < 256; u += 32) {
+    S.w[0][u] = __ldg(wbp + wbase + u);
+    S.w[1][u] = __ldg(wap + wbase + u);
+  }
+  for (int rho = lane; rho < kDRows; rho += 32) {
+    const int row = X - 56 + rho;
+    const bool ok = row >= 0 && row < xend;
+    const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+    for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = ok ? __ldg(src + c) : 0.0;
+  }
+  __syncwarp();
+  chunk_prefetch_next<D>(wbp, wap, Fp, T0, X + kB, xend, lane);
+  const int i = lane >> 2, k = lane & 3;
+  const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
+#pragma unroll 2
+  for (int v = 0; v < nsteps; ++v) {
+    const int sbr = 4 * v;
+    double a[2][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = 64 * h + i - k + 183 - sbr;
+      a[h][0] = S.w[0][u];
+      a[h][1] = S.w[1][u];
+    }
+    const int rho = sbr + k + 8 * i;
+    double b[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+  }
+}
+
+// batched staging: every load of the chunk issued before any shared store
+template <int D>
+__device__ __forceinline__ void dmma_chunk_batched(const double* __restrict__ wbp, const double* __restrict__ wap,
+                                                   const double* __restrict__ Fp, DmmaSmem<D>& S, int T0, int X,
+                                                   int xend, int lane, DmmaAcc<D>& acc) {
+  constexpr int DS = Stride<D>::value;
+  const long long wbase = static_cast<long long>(T0) - X - 127;
+  double wv[2][8], fv[6][D];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    wv[0][q] = __ldg(wbp + wbase + lane + 32 * q);
+    wv[1][q] = __ldg(wap + wbase + lane + 32 * q);
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int rho = lane + 32 * q;
+    const int row = X - 56 + rho;
+    const bool ok = rho < kDRows && row >= 0 && row < xend;
+    const double* src = Fp + static_cast<long long>(ok ? row : 0) * DS;
+#pragma unroll
+    for (int c = 0; c < D; ++c) fv[q][c] = ok ? __ldcg(src + c) : 0.0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    S.w[0][lane + 32 * q] = wv[0][q];
+    S.w[1][lane + 32 * q] = wv[1][q];
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int rho = lane + 32 * q;
+    if (rho < kDRows) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) S.f[c][dmma_fidx(rho)] = fv[q][c];
+    }
+  }
+  __syncwarp();
+  const int i = lane >> 2, k = lane & 3;
+  const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
+#pragma unroll 2
+  for (int v = 0; v < nsteps; ++v) {
+    const int sbr = 4 * v;
+    double a[2][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = 64 * h + i - k + 183 - sbr;
+      a[h][0] = S.w[0][u];
+      a[h][1] = S.w[1][u];
+    }
+    const int rho = sbr + k + 8 * i;
+    double b[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) batched_kernel(const double* wb, const double* wa, const double* F,
+                                                              int chunks, double* out, int active) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= active) return;
+  auto* S = reinterpret_cast<DmmaSmem<D>*>(smem_raw) + warp;
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
+  const int J = chunks + kL + (blockIdx.x * kWarps + warp) % 64;
+  for (int I = 0; I < chunks; ++I)
+    dmma_chunk_batched<D>(wb, wa, F, *S, J * kB, I * kB, (J - kL + 1) * kB, lane, acc);
+  double s = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) s += acc[h][c][w][0] + acc[h][c][w][1];
+  out[blockIdx.x * kThreads + threadIdx.x] = s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) pf_kernel(const double* wb, const double* wa, const double* F,
+                                                         int chunks, double* out, int active) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= active) return;
+  auto* S = reinterpret_cast<DmmaSmem<D>*>(smem_raw) + warp;
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
+  const int J = chunks + kL + (blockIdx.x * kWarps + warp) % 64;
+  for (int I = 0; I < chunks; ++I) dmma_chunk_pf<D>(wb, wa, F, *S, J * kB, I * kB, (J - kL + 1) * kB, lane, acc);
+  double s = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) s += acc[h][c][w][0] + acc[h][c][w][1];
+  out[blockIdx.x * kThreads + threadIdx.x] = s;
+}
+
+// sweep-only: stage one chunk, sweep it `chunks` times (no restaging) -- the
+// DMMA sweep's own ceiling for k warps per SM
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) sweep_kernel(const double* wb, const double* wa, const double* F,
+                                                            int chunks, double* out, int active) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= active) return;
+  auto* S = reinterpret_cast<DmmaSmem<D>*>(smem_raw) + warp;
+  DmmaAcc<D> acc;
+  dmma_zero<D>(acc);
+  const int J = chunks + kL + 8;
+  DmmaAcc<D> tmp;
+  dmma_zero<D>(tmp);
+  dmma_chunk<D>(wb, wa, F, *S, J * kB, 0, (J - kL + 1) * kB, lane, tmp);  // stage chunk 0
+  const int i = lane >> 2, k = lane & 3;
+  for (int I = 0; I < chunks; ++I) {
+#pragma unroll 2
+    for (int v = 0; v < kDSweep; ++v) {
+      const int sbr = 4 * v;
+      double a[2][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = 64 * h + i - k + 183 - sbr;
+        a[h][0] = S->w[0][u];
+        a[h][1] = S->w[1][u];
+      }
+      const int rho = sbr + k + 8 * i;
+      double b[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) b[c] = S->f[c][dmma_fidx(rho)];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+#pragma unroll
+          for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+    }
+  }
+  double s = tmp[0][0][0][0];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) s += acc[h][c][w][0] + acc[h][c][w][1];
+  out[blockIdx.x * kThreads + threadIdx.x] = s;
+}
+
 // variant: the two weight windows staged by TMA bulk copies (one elected
 // lane, mbarrier completion), the f rows by the lanes as in dmma_chunk
 template <int D>
@@ -160,6 +379,64 @@ int main() {
     }
     const double f1 = (double)nsm * active * chunks * 2.0 * kB * kB * D;
     printf("  %2d warp(s)/SM: %.4e FMA/s = %.3f of the 16-warp rate per SM\n", active, f1 / (tb * 1e-3),
+           (f1 / (tb * 1e-3)) / (fma / (best * 1e-3)));
+  }
+  cudaFuncSetAttribute(pf_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int active : {1, 2, 4, 8, 16}) {
+    float tb = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0);
+      pf_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out, active);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tb = ms < tb ? ms : tb;
+    }
+    const double f1 = (double)nsm * active * chunks * 2.0 * kB * kB * D;
+    printf("  L1 prefetch of the next chunk, %2d warp(s)/SM: %.4e FMA/s = %.3f of the 16-warp chunk rate\n", active,
+           f1 / (tb * 1e-3), (f1 / (tb * 1e-3)) / (fma / (best * 1e-3)));
+  }
+  cudaFuncSetAttribute(batched_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int active : {1, 4, 8, 16}) {
+    float tb = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0);
+      batched_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out, active);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tb = ms < tb ? ms : tb;
+    }
+    const double f1 = (double)nsm * active * chunks * 2.0 * kB * kB * D;
+    printf("  batched staging loads, %2d warp(s)/SM: %.4e FMA/s = %.3f of the 16-warp chunk rate\n", active,
+           f1 / (tb * 1e-3), (f1 / (tb * 1e-3)) / (fma / (best * 1e-3)));
+  }
+  {
+    std::vector<double> r1(nsm * kThreads), r2(nsm * kThreads);
+    chunk_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out);
+    cudaMemcpy(r1.data(), out, 8 * r1.size(), cudaMemcpyDeviceToHost);
+    batched_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out, kWarps);
+    cudaMemcpy(r2.data(), out, 8 * r2.size(), cudaMemcpyDeviceToHost);
+    bool same = true;
+    for (size_t q = 0; q < r1.size(); ++q) same &= r1[q] == r2[q];
+    printf("  batched staging bitwise %s\n", same ? "equal" : "DIFFERENT");
+  }
+  cudaFuncSetAttribute(sweep_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int active : {1, 4, 16}) {
+    float tb = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0);
+      sweep_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out, active);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      tb = ms < tb ? ms : tb;
+    }
+    const double f1 = (double)nsm * active * chunks * 2.0 * kB * kB * D;
+    printf("  sweep only, %2d warp(s)/SM: %.4e FMA/s = %.3f of the 16-warp chunk rate\n", active, f1 / (tb * 1e-3),
            (f1 / (tb * 1e-3)) / (fma / (best * 1e-3)));
   }
   chunk_kernel<D><<<nsm, kThreads, smem>>>(wb, wa, F, chunks, out);
