@@ -114,9 +114,9 @@ __device__ __forceinline__ void dmma_chunk(const double* __restrict__ wbp, const
     __syncwarp();
   }
   const int i = lane >> 2, k = lane & 3;
-  const int nsteps = (X + 128 >= xend) ? kDSweep + kDClose : kDSweep;
-#pragma unroll 2
-  for (int v = 0; v < nsteps; ++v) {
+  // the 32 regular sweep steps read staged rows only (rho <= 183); the
+  // closing steps of a target's last chunk run past them and read zeros
+  auto step = [&](int v, bool guard) {
     const int sbr = 4 * v;  // sb - (X - 56)
     // A = W[tb + i - sb - k], tb = T0 + 64 h  ->  u = 64 h + i - k + 183 - sbr
     double a[2][2];
@@ -126,18 +126,23 @@ __device__ __forceinline__ void dmma_chunk(const double* __restrict__ wbp, const
       a[h][0] = S.w[0][u];
       a[h][1] = S.w[1][u];
     }
-    // B = f[sb + k + 8j], column j = lane >> 2; rows past the staged range
-    // (closing sweep) are zero
+    // B = f[sb + k + 8j], column j = lane >> 2
     const int rho = sbr + k + 8 * i;
     double b[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) b[c] = rho < kDRows ? S.f[c][dmma_fidx(rho)] : 0.0;
+    for (int c = 0; c < D; ++c) b[c] = (!guard || rho < kDRows) ? S.f[c][dmma_fidx(rho)] : 0.0;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int c = 0; c < D; ++c)
 #pragma unroll
         for (int w = 0; w < 2; ++w) dmma_f64(acc[h][c][w][0], acc[h][c][w][1], a[h][w], b[c]);
+  };
+#pragma unroll 2
+  for (int v = 0; v < kDSweep; ++v) step(v, false);
+  if (X + 128 >= xend) {
+#pragma unroll 1
+    for (int v = kDSweep; v < kDSweep + kDClose; ++v) step(v, true);
   }
 }
 
