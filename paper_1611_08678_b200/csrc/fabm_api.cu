@@ -810,7 +810,10 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   }
   // pull segments: G source blocks per pull unit (batch.cuh); the ticket
   // layout of round J is T * S_J pulls then T steps, S_J = ceil(J / G)
-  constexpr int kPullG = 32;
+#ifndef FABM_BATCH_G
+#define FABM_BATCH_G 32
+#endif
+  constexpr int kPullG = FABM_BATCH_G;
   const int S_max = std::max(1, (nb - 1 + kPullG - 1) / kPullG);
   std::vector<long long> hround(nb + 1, 0);
   for (int J = 0; J < nb; ++J) hround[J + 1] = hround[J] + static_cast<long long>(T) * ((J + kPullG - 1) / kPullG + 1);
