@@ -1,4 +1,4 @@
-"""Small invocations of every device entry point (a driver for compute-sanitizer where it is available;
+"""Small invocations of every device entry point (also a driver for compute-sanitizer where the pool allows it;
   compute-sanitizer --tool memcheck  python tools/sanitize.py
   compute-sanitizer --tool synccheck python tools/sanitize.py
 (race detection / sanitizers on small N)."""
