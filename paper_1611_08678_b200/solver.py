@@ -267,29 +267,54 @@ class _PinnedPool:
     reference (serial.py:55-56)."""
 
     def __init__(self, keep_bytes: int = 1 << 31):
+        import collections
         import threading
 
         self.keep_bytes = keep_bytes
         self.free: dict[int, list[int]] = {}
         self.kept = 0
         self.lock = threading.Lock()
+        # buffers handed back by finalizers.  A finalizer runs whenever the
+        # garbage collector does -- possibly inside take() on this thread,
+        # with the lock held -- so it only appends here (atomic, no lock);
+        # take() and drain() move the entries into the free lists.
+        self.returned: "collections.deque[tuple[int, int]]" = collections.deque()
 
-    def take(self, nbytes: int) -> int | None:
-        with self.lock:
-            lst = self.free.get(nbytes)
-            if lst:
-                self.kept -= nbytes
-                return lst.pop()
-        ptr = nat.load().fabm_host_alloc(nbytes)
-        return int(ptr) if ptr else None
-
-    def give(self, nbytes: int, ptr: int):
-        with self.lock:
+    def _drain_locked(self) -> list[int]:
+        excess = []
+        while self.returned:
+            nbytes, ptr = self.returned.popleft()
             if self.kept + nbytes <= self.keep_bytes:
                 self.free.setdefault(nbytes, []).append(ptr)
                 self.kept += nbytes
-                return
-        nat.load().fabm_host_free(ptr)
+            else:
+                excess.append(ptr)
+        return excess
+
+    def take(self, nbytes: int) -> int | None:
+        with self.lock:
+            excess = self._drain_locked()
+            lst = self.free.get(nbytes)
+            ptr = lst.pop() if lst else None
+            if ptr is not None:
+                self.kept -= nbytes
+        lib = nat.load()
+        for p in excess:
+            lib.fabm_host_free(p)
+        if ptr is not None:
+            return ptr
+        ptr = lib.fabm_host_alloc(nbytes)
+        return int(ptr) if ptr else None
+
+    def give(self, nbytes: int, ptr: int):
+        self.returned.append((nbytes, ptr))
+
+    def drain(self) -> list[int]:
+        """Empty the pool; returns the pointers for the caller to free."""
+        with self.lock:
+            excess = self._drain_locked()
+            free, self.free, self.kept = self.free, {}, 0
+        return excess + [p for ptrs in free.values() for p in ptrs]
 
     def array(self, rows: int, cols: int) -> np.ndarray | None:
         import weakref
@@ -340,12 +365,9 @@ def release_cached_memory(device: int | None = None) -> None:
     batch solver allocates from (on ``device``, default: every device)."""
     while _PLAN_CACHE:
         _PLAN_CACHE.popitem(last=False)[1].close()
-    with _PINNED.lock:
-        free, _PINNED.free, _PINNED.kept = _PINNED.free, {}, 0
     lib = nat.load()
-    for ptrs in free.values():
-        for ptr in ptrs:
-            lib.fabm_host_free(ptr)
+    for ptr in _PINNED.drain():
+        lib.fabm_host_free(ptr)
     for dev in ([device] if device is not None else range(int(lib.fabm_device_count()))):
         lib.fabm_trim_memory(int(dev))
 

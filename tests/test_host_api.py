@@ -268,10 +268,16 @@ class TestPinnedPool:
         b = pool.take(64)
         assert allocs == [64, 64] and a != b
         pool.give(64, a)
-        assert pool.kept == 64 and pool.take(64) == a and pool.kept == 0
+        assert pool.take(64) == a and pool.kept == 0
         pool.give(64, a)
         pool.give(64, b)  # over the cap: released, not kept
-        assert frees == [b] and pool.kept == 64
+        c = pool.take(32)
+        assert frees == [b] and pool.kept == 64 and allocs == [64, 64, 32]
+        # a finalizer may run inside take() with the lock held (the garbage
+        # collector fires on any allocation): give() must not block on it
+        with pool.lock:
+            pool.give(32, c)
+        assert sorted(pool.drain()) == sorted([a, c]) and pool.kept == 0
 
 
 def test_write_trajectory_npz_round_trip(tmp_path):
