@@ -66,6 +66,8 @@ def parse():
                     help="lorenz: headline single trajectory (default); batch: BASELINE config 4 alpha sweep; "
                          "sharded: config 5; csv: the trajectory CSV of the headline solve (SURVEY 8f row 2)")
     ap.add_argument("--batch-size", type=int, default=4096, help="trajectories in the config 4 sweep")
+    ap.add_argument("--no-subrecords", action="store_true",
+                    help="skip the config-4 / config-5 sub-records of the default line")
     return ap.parse_args()
 
 
@@ -174,6 +176,7 @@ def cpu_baseline(n_target: int, budget_s: float) -> dict:
                    f"{threads} OpenMP threads, Lorenz prefixes M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s) of the "
                    f"N={n_target} run; projected t(N)=a*N+c*N^2 = {t_full:.1f}s"),
         "projected_seconds": t_full,
+        "prefixes": [[m1, round(t1, 4)], [m2, round(t2, 4)]],
         "cpu_model": _cpu_model(),
     }
 
@@ -227,13 +230,16 @@ def run_reference(args, world, rank):
     budget = args.cpu_seconds
     times = []
     info = None
+    prefix_log = []
     for i in range(args.warmup + args.steps):
         info = cpu_baseline(n, budget / 2)
         if i >= args.warmup:
             times.append(info["projected_seconds"])
+            prefix_log.append(info["prefixes"])
     t_full = statistics.median(times)
     value = n / t_full
     extra = reference_python_sample(n)
+    par = reference_parallel_sample(n)
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -252,9 +258,18 @@ def run_reference(args, world, rank):
                    "system": "lorenz", "alpha": ALPHA, "t_end": T_END},
         "cpu_baseline": {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # every "step" of this arm is a PROJECTION: two prefix solves of the
+        # C port, extrapolated with t = a*N + c*N^2 -- not a full N=1e6 solve
+        # (which takes minutes on the host CPU)
+        "projected": True,
+        "step_definition": ("one step = the C port on the Lorenz prefixes M1 and M2 of the N=1e6 run (all host "
+                            "threads), projected to N with the fitted t = a*N + c*N^2"),
+        "prefix_seconds": prefix_log,
     }
     if extra is not None:
         out["reference_python_serial"] = extra
+    if par is not None:
+        out["reference_parallel"] = par
     print(json.dumps(out))
 
 
@@ -292,6 +307,48 @@ def reference_python_sample(n_target: int) -> dict | None:
                            f"and M={m2} ({t2:.2f}s); projected t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}")}
     except Exception as exc:  # noqa: BLE001 - informational only
         return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+def reference_parallel_sample(n_target: int) -> dict | None:
+    """The reference's own parallel CPU strategies (fodeabm.solve_block_parallel,
+    parallel/block.py:44-236, and solve_reduction_parallel, reduction.py:139-354)
+    at P = all host cores, unmodified, on Lorenz prefixes of the headline run,
+    projected to N with t = a*N + c*N^2.  Only when the
+    reference is installed at baseline/_ref."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "fodeabm").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    out = {}
+    try:
+        import fodeabm
+
+        P = os.cpu_count() or 1
+        sigma, rho, beta = 10.0, 28.0, 8.0 / 3.0
+
+        def lorenz(t, y):
+            return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
+
+        h = T_END / N_STEPS
+        for name, fn in (("block", fodeabm.solve_block_parallel), ("reduction", fodeabm.solve_reduction_parallel)):
+            samples = []
+            for m in (20000, 40000):
+                prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
+                t0 = time.perf_counter()
+                fn(prob, fodeabm.GridSpec(n_steps=m, h=h), P)
+                samples.append((m, time.perf_counter() - t0))
+            (m1, t1), (m2, t2) = samples
+            c = (t2 / m2 - t1 / m1) / (m2 - m1)
+            a = max(t1 / m1 - c * m1, 0.0)
+            t_full = a * n_target + c * n_target * n_target
+            out[name] = {"value": n_target / t_full, "unit": UNIT, "cores": P, "kind": "reference", "projected": True,
+                         "sample": (f"fodeabm.solve_{name}_parallel (baseline/_ref, unmodified) P={P} workers, "
+                                    f"Lorenz prefixes M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s); projected "
+                                    f"t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}")}
+    except Exception as exc:  # noqa: BLE001 - informational only
+        out["error"] = f"{type(exc).__name__}: {exc}"
+    return out
 
 
 def run_fabm(args, world, rank, local):
@@ -354,11 +411,13 @@ def run_fabm(args, world, rank, local):
     hist_fma = 3.0 * n * n
     achieved_tflops = 2.0 * hist_fma / (mean_ms * 1e-3) / 1e12
     peak_tflops = 2.0 * peak_fma / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "engine_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(prof.read_text())
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_src = f"profiles/engine_traffic.json ({tj.get('source', 'ncu capture')}), not measured in this run"
         except (OSError, ValueError):
             traffic = None
 
@@ -371,6 +430,14 @@ def run_fabm(args, world, rank, local):
         dist.all_gather(buf, t)
         gathered = [b.cpu().tolist() for b in buf]
 
+    plan.close()
+    # the north-star multi-GPU workloads, at this N: the
+    # config-4 alpha sweep sharded over the ranks, and the config-5 single
+    # N=1e7 trajectory with its history sharded over the ranks
+    subs = {}
+    if not args.no_subrecords:
+        subs["batch_sweep"] = sub_batch_sweep(args, world, rank, local)
+        subs["sharded"] = sub_sharded(args, world, rank, local)
     if rank != 0:
         return
     cpu = None
@@ -404,6 +471,7 @@ def run_fabm(args, world, rank, local):
             "unit": "TFLOP/s",
             "frac": achieved_tflops / peak_tflops,
             "traffic": traffic,
+            "traffic_source": traffic_src,
             "note": ("history FP64 FMA pipe: 2*d*N^2 algorithmic flop per solve over the engine kernel time; "
                      "peak = DFMA microbenchmark measured live (MEASURED_PEAKS.json has no FP64 entry)"),
         },
@@ -414,9 +482,130 @@ def run_fabm(args, world, rank, local):
         "engine": {"kernel_ms": kernel_ms, "wall_s": wall, "bulk_ctas": stats["bulk_ctas"],
                    "bulk_tiles": stats["bulk_tiles"], "leader_wait_ms": stats["leader_wait_ns"] / 1e6,
                    "block": stats["block"], "window_blocks": stats["window_blocks"],
-                   "y_N": y_last.tolist(), "gathered_y_N": gathered},
+                   "y_N": y_last.tolist(), "gathered_y_N": gathered,
+                   "bulk_claims": stats.get("bulk_claims"), "segment_max": stats.get("segment")},
     }
+    out.update(subs)
     print(json.dumps(out))
+
+
+def _guarded(world, fn):
+    """Run a sub-record on every rank; an exception anywhere becomes an error
+    record on every rank (the collectives stay aligned, the bench line is
+    still printed)."""
+    err = None
+    res = None
+    try:
+        res = fn()
+    except Exception as exc:  # noqa: BLE001
+        err = f"{type(exc).__name__}: {exc}"
+    if world > 1:
+        import torch.distributed as dist
+
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        bad = [e for e in errs if e]
+        if bad:
+            return {"error": bad[0]}
+    elif err:
+        return {"error": err}
+    return res
+
+
+def sub_batch_sweep(args, world, rank, local, reps: int = 2):
+    """BASELINE config 4 through the public sharded call
+    (parallel.solve_batch_distributed): 4096 financial trajectories, alpha =
+    0.9 + 0.1 i/4096, N=1e5, T=100, sliced over the ranks; the kernel time is
+    the max over ranks, y_N of the whole sweep is all-gathered."""
+    import paper_1611_08678_b200 as fabm
+    from paper_1611_08678_b200 import parallel
+
+    T, n = 4096, 100_000
+    rhs = fabm.rhs_financial()
+    probs = [fabm.FractionalProblem(alpha=0.9 + 0.1 * i / T, dim=3, rhs=rhs, y0=(2.0, 3.0, 2.0), t_end=100.0)
+             for i in range(T)]
+    grid = fabm.GridSpec(n_steps=n, h=100.0 / n)
+
+    def body():
+        parallel.solve_batch_distributed(probs, grid, device=local)  # warm-up
+        kms, walls, y_all = [], [], None
+        for _ in range(reps):
+            barrier(world)
+            t0 = time.perf_counter()
+            y_all, res = parallel.solve_batch_distributed(probs, grid, device=local)
+            walls.append(time.perf_counter() - t0)
+            kms.append(res.kernel_ms if res is not None else 0.0)
+        return kms, walls, y_all
+
+    r = _guarded(world, body)
+    if isinstance(r, dict):
+        return r
+    kms, walls, y_all = r
+    step_ms = max_over_ranks(world, float(np.mean(kms)))
+    wall_s = max_over_ranks(world, float(np.mean(walls)))
+    if rank != 0:
+        return None
+    peak = 2.0 * fabm.measure_dfma_peak(local) / 1e12
+    fma = 3.0 * n * n * T
+    achieved = 2.0 * fma / (step_ms * 1e-3) / 1e12 / world
+    return {"metric": "trajectory-steps/s, financial alpha sweep 4096 x N=1e5 (BASELINE config 4)",
+            "value": T * n / (step_ms * 1e-3), "unit": "steps/s", "ms_per_sweep": step_ms, "reps": reps,
+            "scaling": "strong", "parallelism": f"trajectory slices x{world}, NCCL all-gather of y_N",
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s per GPU",
+                         "frac": achieved / peak},
+            "e2e": {"value": T * n / wall_s, "unit": "steps/s",
+                    "note": "parallel.solve_batch_distributed wall time (host problems in, gathered y_N out)"},
+            "y_N_checksum": float(np.sum(y_all)), "y_N_first": y_all[0].tolist(), "y_N_last": y_all[-1].tolist()}
+
+
+def sub_sharded(args, world, rank, local, reps: int = 1):
+    """BASELINE config 5 through the public collective call
+    (parallel.solve_sharded): ONE fractional Lorenz trajectory, alpha 0.99,
+    h=1e-4, N=1e7, its bulk units computed by the GPUs of all ranks (one GPU:
+    the plain engine).  Kernel time is the max over ranks."""
+    import paper_1611_08678_b200 as fabm
+    from paper_1611_08678_b200 import parallel
+
+    n, h = 10_000_000, 1e-4
+    prob = fabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=fabm.rhs_lorenz(), y0=Y0, t_end=n * h)
+    grid = fabm.GridSpec(n_steps=n, h=h)
+
+    def body():
+        kms, walls, y_n = [], [], None
+        for i in range(1 + reps):  # the first solve is the warm-up
+            st = {}
+            barrier(world)
+            t0 = time.perf_counter()
+            traj = parallel.solve_sharded(prob, grid, device=local, stats=st)
+            wall = time.perf_counter() - t0
+            if i:
+                kms.append(st.get("kernel_ms", 0.0))
+                walls.append(wall)
+            if traj is not None:
+                y_n = traj.states[-1].tolist()
+            del traj
+        return kms, walls, y_n, st
+
+    r = _guarded(world, body)
+    if isinstance(r, dict):
+        return r
+    kms, walls, y_n, st = r
+    step_ms = max_over_ranks(world, float(np.mean(kms)))
+    wall_s = max_over_ranks(world, float(np.mean(walls)))
+    if rank != 0:
+        return None
+    peak = 2.0 * fabm.measure_dfma_peak(local) / 1e12
+    achieved = 2.0 * 3.0 * n * n / (step_ms * 1e-3) / 1e12 / world
+    return {"metric": "steps/s, one fractional Lorenz trajectory N=1e7 (BASELINE config 5)",
+            "value": n / (step_ms * 1e-3), "unit": "steps/s", "ms_per_solve": step_ms, "reps": reps,
+            "scaling": "strong", "parallelism": (f"bulk units over {world} GPUs (CUDA IPC arenas over NVLink)"
+                                                 if world > 1 else "one GPU"),
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s per GPU",
+                         "frac": achieved / peak},
+            "e2e": {"value": n / wall_s, "unit": "steps/s",
+                    "note": "parallel.solve_sharded wall time incl. plan setup and the 480 MB trajectory D2H"},
+            "leader_wait_ms": st.get("leader_wait_ns", 0) / 1e6, "bulk_claims": st.get("bulk_claims"),
+            "y_N": y_n}
 
 
 def run_batch(args, world, rank, local):

@@ -119,7 +119,8 @@ typedef struct fabm_stats {
   int32_t bulk_ctas;       /* CTAs running bulk agents                          */
   int32_t block;           /* history block B                                   */
   int32_t window_blocks;   /* stepper window L (blocks)                         */
-  int32_t reserved;
+  int32_t segment;         /* source blocks per bulk unit (fixed by n_steps)    */
+  int64_t bulk_claims;     /* bulk units computed by an agent other than the owner */
 } fabm_stats;
 
 typedef struct fabm_plan fabm_plan;
@@ -171,6 +172,14 @@ int fabm_plan_set_host_output(fabm_plan* plan, double* states, double* f_cache,
                               fabm_status* status);
 void* fabm_host_alloc(int64_t bytes);   /* mapped, portable pinned memory; NULL on failure */
 void fabm_host_free(void* ptr);
+
+/* Cap the bulk-agent CTAs of the next runs (n_ctas <= 0: the default, one
+ * CTA per SM besides the stepper).  Results do not depend on it (the unit
+ * partition and the reduction order depend on n_steps only); the parity
+ * tests use it to put many target blocks on each agent at small n_steps.
+ * No reference counterpart (the reference's worker count, parallel/block.py:
+ * 44-51, sets its partition instead). */
+int fabm_plan_set_bulk_ctas(fabm_plan* plan, int n_ctas, fabm_status* status);
 
 /* Zero the run flags of a plan.  fabm_plan_run does this itself, except on a
  * plan attached to peer shards: there every rank calls fabm_plan_reset, then

@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_stats",
     "fabm_plan_destroy",
     "fabm_plan_reset",
+    "fabm_plan_set_bulk_ctas",
     "fabm_plan_ipc_handle",
     "fabm_plan_attach_shards",
     "fabm_plan_set_virtual_shards",
@@ -113,11 +114,12 @@ class Stats(ctypes.Structure):
         ("bulk_ctas", ctypes.c_int32),
         ("block", ctypes.c_int32),
         ("window_blocks", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("segment", ctypes.c_int32),
+        ("bulk_claims", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        return {name: getattr(self, name) for name, _ in self._fields_}
 
 
 _DP = ctypes.POINTER(ctypes.c_double)
@@ -143,6 +145,7 @@ def _declare(lib):
         "fabm_plan_stats": (ctypes.c_int, [plan, St]),
         "fabm_plan_destroy": (None, [plan]),
         "fabm_plan_reset": (ctypes.c_int, [plan, S]),
+        "fabm_plan_set_bulk_ctas": (ctypes.c_int, [plan, ctypes.c_int, S]),
         "fabm_plan_ipc_handle": (ctypes.c_int, [plan, ctypes.c_void_p, S]),
         "fabm_plan_attach_shards": (ctypes.c_int, [plan, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, S]),
         "fabm_plan_set_virtual_shards": (ctypes.c_int, [plan, ctypes.c_int, S]),
@@ -165,7 +168,11 @@ def _declare(lib):
                                                ctypes.POINTER(ctypes.c_int32), S]),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:
+            if os.environ.get("FABM_LIBRARY"):  # dev A/B against an older build (tools/ab_engine.py)
+                continue
+            raise RuntimeError(f"libfabm is missing the entry point {name} (stale build?)")
         fn.restype = res
         fn.argtypes = args
 

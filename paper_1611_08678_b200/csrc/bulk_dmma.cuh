@@ -184,6 +184,30 @@ __device__ __forceinline__ void dmma_reload(const double* BK, int J, int lane, D
         acc[h][c][w][1] = v.y;
       }
 }
+// a unit's partial-sum slot (lane-major, 8D doubles per lane)
+template <int D>
+__device__ __forceinline__ void dmma_spill_slot(double* slot, int lane, const DmmaAcc<D>& acc) {
+  dmma_spill<D>(slot, 0, lane, acc);
+}
+template <int D>
+__device__ __forceinline__ void dmma_reload_slot(const double* slot, int lane, DmmaAcc<D>& acc) {
+  dmma_reload<D>(slot, 0, lane, acc);
+}
+// acc += slot, element by element (the fixed-order reduction of partials)
+template <int D>
+__device__ __forceinline__ void dmma_add_slot(const double* slot, int lane, DmmaAcc<D>& acc) {
+  const double* src = slot + lane * (8 * D);
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(src) + (h * D + c) * 2 + w);
+        acc[h][c][w][0] = __dadd_rn(acc[h][c][w][0], v.x);
+        acc[h][c][w][1] = __dadd_rn(acc[h][c][w][1], v.y);
+      }
+}
 // final sums in the row layout the stepper stages: BK[(J B + t) 2 DS + w DS + c]
 template <int D>
 __device__ __forceinline__ void dmma_store_rows(double* BK, int J, int lane, const DmmaAcc<D>& acc) {

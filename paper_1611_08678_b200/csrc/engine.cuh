@@ -25,6 +25,18 @@
 #pragma once
 #include "device_common.cuh"
 
+// code-generation boundaries between the warp roles (register allocation
+// of one role must not depend on another's code)
+#ifndef FABM_NI_LEADER
+#define FABM_NI_LEADER
+#endif
+#ifndef FABM_NI_AGENT
+#define FABM_NI_AGENT
+#endif
+#ifndef FABM_NI_OTHERS
+#define FABM_NI_OTHERS
+#endif
+
 namespace fabm {
 
 // ------------------------------------------------------------ geometry
@@ -63,8 +75,9 @@ struct DevCtrl {
   unsigned long long leader_wait_ns;
   unsigned long long bulk_tiles;
   unsigned long long leader_throttle_ns;
+  unsigned long long bulk_claims;  // units taken by a claimer (not their owner)
   unsigned long long prof[8];  // FABM_PROFILE builds: leader phase cycles
-  int pad2[16];
+  int pad2[14];
 };
 
 // One shard = the bulk agents of one GPU.  Every shard holds a full copy of
@@ -107,6 +120,16 @@ struct EngineParams {
   int agent_cta_base;      // global index of this launch's first agent CTA
   int n_agent_ctas;        // agent CTAs over all shards
   const ShardView* shard;  // device table of n_shards views (global memory: indexed at run time)
+  int has_stepper;         // CTA 0 of this launch is the stepper (every launch but a real shard > 0)
+  // bulk units (shard 0's arena): per-unit claim words and partial-sum
+  // slots, per-target counts of finished non-final units and of stage-2
+  // arrivals, per-(class, column) claim cursors
+  int k_max;               // highest segment class of this run
+  int* claim;
+  int* tdone;
+  int* tstage;
+  int* col_next;           // [kMaxClasses][32]
+  double* PK;
 };
 
 __device__ __forceinline__ long long lo_of(long long m) {
@@ -387,7 +410,7 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
 }
 
 template <int SYS, int D>
-__device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) {
+FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) {
   const long long N = P.N;
   LeaderState<D> st;
   double f0[D];
@@ -561,7 +584,7 @@ __device__ __forceinline__ void helper_batch(const StepperSmem& S, int k0, int k
 }
 
 template <int D>
-__device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, int hwarp) {
+FABM_NI_OTHERS __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, int hwarp) {
   constexpr int NS = kSlotsPerThread;
   const int N = static_cast<int>(P.N);
   const int lane = threadIdx.x & 31;
@@ -648,7 +671,7 @@ __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, i
 // of 32 steps; after the last row of a source block it raises io_block (CTA
 // scope, release).  It never touches slow global state, so it keeps pace.
 template <int D>
-__device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) {
+FABM_NI_OTHERS __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) {
   constexpr int DS = Stride<D>::value;
   const long long N = P.N;
   long long k0 = 0;
@@ -726,7 +749,7 @@ __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) 
 // from HBM into shared memory for the helpers.  All slow global round trips
 // of the stepper CTA live here, off the writer's and the leader's paths.
 template <int D>
-__device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lane) {
+FABM_NI_OTHERS __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lane) {
   constexpr int DS = Stride<D>::value;
   const int nb = P.nb;
   const int last_block = static_cast<int>(P.N / kB);  // complete source blocks at the end
@@ -846,35 +869,196 @@ __device__ void stepper_cta(const EngineParams& P, StepperSmem& S) {
 #include "bulk_dmma.cuh"
 namespace fabm {
 
-// Round-robin ownership: agent a owns targets J = L + a + i*nA, so every
-// newly completed source block brings each agent about the same number of
-// tiles (one per owned target above it).
+// ---------------------------------------------------------------- units
+// The bulk sums of target block J run over its n = J-L+1 chunks I = 0 .. J-L
+// (Toeplitz tiles T_{J-I} F_I).  The chunks are cut at fixed points into
+// SEGMENTS of S = 2^k chunks, k = max(0, floor(log2 n) - 4), so a target has
+// 16..32 units (fewer below n = 16): unit (J, s) = chunks [sS, min((s+1)S, n)).
+// A unit is one ascending DMMA chain from zero; a target's sum is its
+// units' partial sums added in ascending s (one fixed-order reduction per
+// target block).  The partition depends on J alone: results are bitwise
+// independent of N (the first M steps of an N-step run equal the M-step
+// run), of which agent or GPU computed which unit, and of the timing.
+//
+// Scheduling: agent a OWNS targets J = L + a + i*A
+// (round-robin) and processes their units incrementally as source blocks
+// are published, earliest target first.  A unit of a COMPLETE column (its
+// segment's sources all published) that no owner has started is CLAIMED by
+// any agent whose earliest owned work is later: targets with the same S
+// form a class, each (class, segment) column has a cursor walking its
+// targets in ascending J, and a per-unit claim word (CAS) arbitrates between
+// owners and claimers.  Reduction in two stages so that the deadline path is
+// short: the last non-final unit to finish sums the prefix p_0 + .. +
+// p_{n-2} (usually long before the deadline), and whichever of {prefix,
+// final unit} arrives second adds the final unit's partial.
+constexpr int kMaxClasses = 32;
+#ifndef FABM_DYN_BURST
+#define FABM_DYN_BURST 4
+#endif
+constexpr int kDynBurst = FABM_DYN_BURST;  // chunks of a claimed unit between selections
+__device__ __forceinline__ int seg_class(int n) {
+  const int k = 31 - __clz(n) - 4;
+  return k > 0 ? k : 0;
+}
+__device__ __forceinline__ int class_lo(int k) { return k == 0 ? 1 : 1 << (k + 4); }  // n range [lo, hi)
+__device__ __forceinline__ int class_hi(int k) { return 1 << (k + 5); }
+__device__ __forceinline__ long long seg_prefix(long long m, int S) {  // sum_{n'=1..m} ceil(n'/S)
+  const long long q = m / S, r = m % S;
+  return static_cast<long long>(S) * q * (q + 1) / 2 + r * (q + 1);
+}
+// units of the classes below k: class 0 (n = 1..31, S = 1) has 496, class
+// j >= 1 (n = 16S..32S-1) has sum_{q=16..31} (qS + S - 1) = 392 S - 16
+__host__ __device__ __forceinline__ long long class_base(int k) {
+  return k == 0 ? 0 : 496 + 392 * ((1LL << k) - 2) - 16LL * (k - 1);
+}
+// unit id of (J, 0): units of targets L .. J-1
+__device__ __forceinline__ long long unit_base(const EngineParams&, int J) {
+  const int n = J - kL + 1;
+  const int k = seg_class(n), S = 1 << k;
+  return class_base(k) + seg_prefix(n - 1, S) - seg_prefix(class_lo(k) - 1, S);
+}
+
 __device__ __forceinline__ int owned_target(int agent, int i, int nA) { return kL + agent + i * nA; }
 __device__ __forceinline__ int owned_count(int agent, int nA, int n_targets) {
   return agent < n_targets ? (n_targets - 1 - agent) / nA + 1 : 0;
 }
 
+__device__ __forceinline__ int at_cas(int* p, int c, int v, bool sys) {
+  return sys ? atomicCAS_system(p, c, v) : atomicCAS(p, c, v);
+}
+__device__ __forceinline__ int at_add(int* p, int v, bool sys) { return sys ? atomicAdd_system(p, v) : atomicAdd(p, v); }
+__device__ __forceinline__ void at_max(int* p, int v, bool sys) {
+  if (sys) atomicMax_system(p, v); else atomicMax(p, v);
+}
+__device__ __forceinline__ int ld_rlx(const int* p, bool sys) { return sys ? ld_relaxed_sys(p) : ld_relaxed_gpu(p); }
+__device__ __forceinline__ void fence_scope(bool sys) {
+  if (sys) __threadfence_system(); else __threadfence();
+}
+
 template <int D>
 struct BulkSmem {
   DmmaSmem<D> t;
-  int own_next[kMaxOwn];   // next source block per owned target
+  int own_next[kMaxOwn];   // owned target i: (next chunk << 1) | (holds the unit of that chunk)
 };
 
 template <int D>
-__device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
+__device__ __forceinline__ double* unit_slot(const EngineParams& P, long long uid) {
+  return P.PK + uid * (32 * 8 * D);
+}
+
+template <int D>
+__device__ __forceinline__ void publish_target(const EngineParams& P, int J, int lane, const DmmaAcc<D>& acc, bool sys) {
+  __syncwarp();
+  dmma_store_rows<D>(P.BK, J, lane, acc);  // shard 0's BK (peer memory on other GPUs)
+  fence_scope(sys);
+  __syncwarp();
+  if (lane == 0) {
+    if (sys) st_release_sys(&P.ready[J], 1); else st_release_gpu(&P.ready[J], 1);
+  }
+#ifdef FABM_PROFILE
+  if (P.trace && lane == 0) P.trace[4 * J + 1] = global_ns();
+#endif
+}
+
+// second arrival at stage 2 of target J's reduction?
+__device__ __forceinline__ bool stage2_second(const EngineParams& P, int J, int lane, bool sys) {
+  int second = 0;
+  if (lane == 0) second = at_add(&P.tstage[J], 1, sys) == 1;
+  second = __shfl_sync(0xffffffffu, second, 0);
+  if (second) fence_scope(sys);
+  return second != 0;
+}
+
+// A unit's chain is complete (acc = its partial sums).
+template <int D>
+__device__ void unit_finish(const EngineParams& P, int J, int s, long long uid, int lane, DmmaAcc<D>& acc, bool sys) {
+  const int n = J - kL + 1;
+  const int S = 1 << seg_class(n);
+  const int nseg = (n + S - 1) / S;
+  if (nseg == 1) {
+    publish_target<D>(P, J, lane, acc, sys);
+    return;
+  }
+  dmma_spill_slot<D>(unit_slot<D>(P, uid), lane, acc);
+  fence_scope(sys);
+  __syncwarp();
+  const long long base = unit_base(P, J);
+  if (s == nseg - 1) {  // the final unit: P + p_final if the prefix is already there
+    if (!stage2_second(P, J, lane, sys)) return;
+    dmma_add_slot<D>(unit_slot<D>(P, base), lane, acc);  // p_final + P == P + p_final (IEEE add commutes)
+    publish_target<D>(P, J, lane, acc, sys);
+    return;
+  }
+  int last = 0;
+  if (lane == 0) last = at_add(&P.tdone[J], 1, sys) == nseg - 2;
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  fence_scope(sys);
+  if (nseg > 2) {  // prefix p_0 + .. + p_{nseg-2} into unit 0's slot
+    dmma_reload_slot<D>(unit_slot<D>(P, base), lane, acc);
+    for (int q = 1; q < nseg - 1; ++q) dmma_add_slot<D>(unit_slot<D>(P, base + q), lane, acc);
+    __syncwarp();
+    dmma_spill_slot<D>(unit_slot<D>(P, base), lane, acc);
+    fence_scope(sys);
+    __syncwarp();
+  } else {
+    dmma_reload_slot<D>(unit_slot<D>(P, base), lane, acc);
+  }
+  if (!stage2_second(P, J, lane, sys)) return;
+  dmma_add_slot<D>(unit_slot<D>(P, base + nseg - 1), lane, acc);
+  publish_target<D>(P, J, lane, acc, sys);
+}
+
+// earliest claimable unit: the lowest class with a claimable column holds
+// the smallest J (classes are ordered by J).  kc: lowest class not yet
+// exhausted (only grows).  Returns J (or INT_MAX) and sets k/c.
+__device__ __forceinline__ int scan_claimable(const EngineParams& P, int M, int lane, bool sys, int& kc, int& kk,
+                                              int& cc) {
+  const int nend_all = P.nb - kL + 1;  // n < nend_all
+  for (int k = kc; k <= P.k_max; ++k) {
+    const int S = 1 << k;
+    const int nend = min(class_hi(k), nend_all);
+    const int ns = max(class_lo(k), (lane + 1) * S + 1);
+    const bool col = lane < 31 && ns < nend;
+    const int cur = col ? ns + ld_rlx(&P.col_next[k * 32 + lane], sys) : nend;
+    const bool exhausted = cur >= nend;
+    if (__all_sync(0xffffffffu, exhausted)) {
+      if (k == kc) kc = k + 1;
+      continue;
+    }
+    const int myJ = (!exhausted && M >= (lane + 1) * S) ? cur + kL - 1 : 0x7fffffff;
+    const int mn = __reduce_min_sync(0xffffffffu, myJ);
+    if (mn < 0x7fffffff) {
+      kk = k;
+      cc = __ffs(__ballot_sync(0xffffffffu, myJ == mn)) - 1;
+      return mn;
+    }
+    if (M < 2 * S) break;  // no complete column in the classes above
+  }
+  return 0x7fffffff;
+}
+
+template <int D>
+FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
-  if (agent >= n_targets || (P.debug & 8)) return;  // debug 8 (dev): no bulk agents (results invalid)
+  if (n_targets <= 0) return;
+  if (P.debug & 8) return;  // dev: no bulk agents (results invalid; the run reports FABM_ERR_CONFIG)
+  const bool sys = P.n_shards > 1;
   const int nA = P.n_agents;
   const int nown = owned_count(agent, nA, n_targets);
-  if (nown == 0) return;
   for (int i = lane; i < nown; i += 32) A.own_next[i] = 0;
   __syncwarp();
   DmmaAcc<D> acc;
   dmma_zero<D>(acc);
-  int cur = -1, done = 0;
-  unsigned long long tiles = 0;
+  long long cur_uid = -1;           // the unit whose chain is in acc
+  int dJ = -1, ds = 0, dnext = 0;   // claimed (dynamic) unit, if any
+  int kc = 0;                       // lowest class with unclaimed columns
+  int dyn_lb = 0, lb_M = -1;        // cached lower bound of the earliest claimable target (valid for lb_M)
+  unsigned idle_polls = 0;
+  unsigned long long tiles = 0, claims = 0;
   unsigned long long last_progress = global_ns();
+  int last_M = -1;  // the watchdog counts the stepper's progress too (an agent may idle for long)
 
 #ifdef FABM_PROFILE
   long long c_tile = 0, c_idle = 0, c_sw = 0, c_t = clock64();
@@ -882,37 +1066,60 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
 #else
 #define APROF(var)
 #endif
-  while (done < nown) {
+  while (true) {
     int M = 0, ab = 0;
     if (lane == 0) {
-      if (P.n_shards == 1) {
-        M = ld_acquire_gpu(&sv.ctrl->src_done);
-        ab = ld_relaxed_gpu(&sv.ctrl->abort);
-      } else {
-        M = ld_acquire_sys(&sv.ctrl->src_done);
-        ab = ld_relaxed_sys(&sv.ctrl->abort);
-      }
+      M = sys ? ld_acquire_sys(&sv.ctrl->src_done) : ld_acquire_gpu(&sv.ctrl->src_done);
+      ab = ld_rlx(&sv.ctrl->abort, sys);
     }
     M = __shfl_sync(0xffffffffu, M, 0);
     ab = __shfl_sync(0xffffffffu, ab, 0);
     if (ab) return;
+    if (M != last_M) {
+      last_M = M;
+      last_progress = global_ns();
+    }
     __syncwarp();
-    // earliest-deadline owned target with available work
+    // earliest owned target with a published chunk in its current unit
     int best = -1;
     for (int b0 = 0; b0 < nown; b0 += 32) {
       const int i = b0 + lane;
       bool pend = false;
       if (i < nown) {
-        const int J = owned_target(agent, i, nA);
-        const int nx = A.own_next[i];
-        const int lim = min(M, J - kL + 1);
-        pend = nx < lim;
+        const int n = owned_target(agent, i, nA) - kL + 1;
+        const int S = 1 << seg_class(n);
+        const int nx = A.own_next[i] >> 1;
+        const int uhi = min((nx / S + 1) * S, n);
+        pend = nx < min(uhi, M);
       }
       const unsigned bal = __ballot_sync(0xffffffffu, pend);
       if (bal) { best = b0 + __ffs(bal) - 1; break; }
     }
-    if (best < 0) {
+    const int Jo = best >= 0 ? owned_target(agent, best, nA) : 0x7fffffff;
+    // earliest claimable unit; the cursors only grow, so a bound read at
+    // the same M stays a lower bound
+    int Jd = 0x7fffffff, kd = 0, cd = -1;
+    if (dJ >= 0) {
+      Jd = dJ;
+    } else if (Jo > dyn_lb || (M >> kc) != (lb_M >> kc) || lb_M < 0) {
+      // a column of a class >= kc completes only when M crosses a multiple
+      // of its segment length 2^k, k >= kc
+      Jd = scan_claimable(P, M, lane, sys, kc, kd, cd);
+      dyn_lb = Jd;
+      lb_M = M;
+    }
+    const bool take_dyn = Jd < Jo;
+    if (!take_dyn && best < 0) {
+      // nothing to do: finished, or wait for the next source block
+      bool fin = dJ < 0 && kc > P.k_max;
+      for (int b0 = 0; b0 < nown && fin; b0 += 32) {
+        const int i = b0 + lane;
+        const bool od = i >= nown || (A.own_next[i] >> 1) >= owned_target(agent, i, nA) - kL + 1;
+        fin = __all_sync(0xffffffffu, od);
+      }
+      if (fin) break;
       __nanosleep(256);
+      if ((++idle_polls & 63) == 0) lb_M = -1;  // re-scan now and then (exit detection)
       APROF(c_idle)
       if (global_ns() - last_progress > P.timeout_ns) {
         if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, -1, 0.0);
@@ -921,52 +1128,105 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
       continue;
     }
     last_progress = global_ns();
-    const int J = owned_target(agent, best, nA);
-    if (cur != best) {
-      if (cur >= 0) dmma_spill<D>(sv.BK, owned_target(agent, cur, nA), lane, acc);
-      if (A.own_next[best] > 0) {
-        dmma_reload<D>(sv.BK, J, lane, acc);
+    int J, s, nx, hi, lim;
+    if (take_dyn) {
+      if (dJ < 0) {
+        // claim the first unclaimed unit of column (kd, cd) at or after Jd:
+        // 32 candidates read at once, CAS on the first free one
+        const int S = 1 << kd;
+        const int ns = max(class_lo(kd), (cd + 1) * S + 1);
+        const int nend = min(class_hi(kd), nb - kL + 1);
+        const int j = Jd + lane;
+        bool freeu = false;
+        if (j - kL + 1 < nend) freeu = ld_rlx(&P.claim[unit_base(P, j) + cd], sys) == 0;
+        const unsigned fb = __ballot_sync(0xffffffffu, freeu);
+        int got = -1;
+        if (lane == 0) {
+          int* cursor = &P.col_next[kd * 32 + cd];
+          if (fb) {
+            const int jj = Jd + __ffs(fb) - 1;
+            if (at_cas(&P.claim[unit_base(P, jj) + cd], 0, agent + 1, sys) == 0) got = jj;
+            at_max(cursor, (jj - kL + 1) - ns + (got >= 0 ? 1 : 0), sys);
+          } else {
+            at_max(cursor, min(Jd - kL + 1 + 32, nend) - ns, sys);
+          }
+        }
+        got = __shfl_sync(0xffffffffu, got, 0);
+        lb_M = -1;  // re-scan next time
+        if (got < 0) continue;
+        dJ = got;
+        ds = cd;
+        dnext = cd * S;
+        ++claims;
+      }
+      J = dJ;
+      s = ds;
+      nx = dnext;
+      hi = min((s + 1) << seg_class(J - kL + 1), J - kL + 1);
+      lim = hi;  // a complete column: every chunk is published
+    } else {
+      J = Jo;
+      const int n = J - kL + 1;
+      const int S = 1 << seg_class(n);
+      const int v = A.own_next[best];
+      nx = v >> 1;
+      s = nx / S;
+      hi = min((s + 1) * S, n);
+      lim = min(hi, M);
+      if (!(v & 1)) {  // first touch of this unit: claim it (a claimer may hold it)
+        int ok = 0;
+        if (lane == 0) ok = at_cas(&P.claim[unit_base(P, J) + s], 0, agent + 1, sys) == 0;
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        __syncwarp();
+        if (lane == 0) A.own_next[best] = ok ? ((nx << 1) | 1) : (hi << 1);
+        __syncwarp();
+        if (!ok) continue;
+      }
+    }
+    const long long uid = unit_base(P, J) + s;
+    if (uid != cur_uid) {
+      if (cur_uid >= 0) dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
+      const int S = 1 << seg_class(J - kL + 1);
+      if (nx > s * S) {
+        __syncwarp();
+        dmma_reload_slot<D>(unit_slot<D>(P, uid), lane, acc);
       } else {
         dmma_zero<D>(acc);
       }
-      cur = best;
+      cur_uid = uid;
     }
     APROF(c_sw)
-    const int lim = min(M, J - kL + 1);
-    int nx = A.own_next[best];
-    while (nx < lim) {
+    // owned units: re-run the selection when a newer source block arrives;
+    // claimed units: in bursts of kDynBurst chunks (fewer spill/reload
+    // switches between a claimed unit and the owned frontier)
+    const int burst_end = take_dyn ? min(lim, nx + kDynBurst) : lim;
+    while (nx < burst_end) {
       int M2 = 0;
-      if (lane == 0) M2 = P.n_shards == 1 ? ld_relaxed_gpu(&sv.ctrl->src_done) : ld_relaxed_sys(&sv.ctrl->src_done);
+      if (lane == 0) M2 = ld_rlx(&sv.ctrl->src_done, sys);
       dmma_chunk<D>(P.wb, P.wa, sv.F, A.t, J * kB, nx * kB, (J - kL + 1) * kB, lane, acc);
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
-      if (M2 != M) break;  // a newer source block arrived: re-run EDF selection
+      if (!take_dyn && M2 != M) break;  // a newer source block arrived: re-run the selection
     }
     APROF(c_tile)
     __syncwarp();
-    if (lane == 0) A.own_next[best] = nx;
+    if (take_dyn) {
+      dnext = nx;
+    } else if (lane == 0) {
+      A.own_next[best] = nx == hi ? (nx << 1) : ((nx << 1) | 1);
+    }
     __syncwarp();
-    if (nx == J - kL + 1) {
-      __syncwarp();  // every lane's reload of this target's spill precedes the row-layout stores
-      dmma_store_rows<D>(P.BK, J, lane, acc);  // shard 0's BK (peer memory on other GPUs)
-      if (P.n_shards == 1) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release_gpu(&P.ready[J], 1);
-      } else {
-        __threadfence_system();
-        __syncwarp();
-        if (lane == 0) st_release_sys(&P.ready[J], 1);
-      }
-#ifdef FABM_PROFILE
-      if (P.trace && lane == 0) P.trace[4 * J + 1] = global_ns();
-#endif
-      cur = -1;
-      ++done;
+    if (nx == hi) {
+      unit_finish<D>(P, J, s, uid, lane, acc, sys);
+      cur_uid = -1;
+      if (take_dyn) dJ = -1;
     }
   }
-  if (lane == 0) atomicAdd(&sv.ctrl->bulk_tiles, tiles);
+  if (lane == 0) {
+    atomicAdd(&sv.ctrl->bulk_tiles, tiles);
+    atomicAdd(&sv.ctrl->bulk_claims, claims);
+  }
 #ifdef FABM_PROFILE
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[4]), (unsigned long long)c_tile);
@@ -980,16 +1240,17 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
 template <int SYS, int D>
 __global__ void __launch_bounds__(kThreads, 1) abm_engine_kernel(EngineParams P) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  if (blockIdx.x == 0) {
-    if (P.my_shard <= 0) stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
+  // the stepper is CTA 0 of the launch that hosts it (shard 0); the launches
+  // of the other shards are agents only
+  if (P.has_stepper && blockIdx.x == 0) {
+    stepper_cta<SYS, D>(P, *reinterpret_cast<StepperSmem*>(smem_raw));
   } else {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     BulkSmem<D>* A = reinterpret_cast<BulkSmem<D>*>(smem_raw) + warp;
-    const int lcta = blockIdx.x - 1;
+    const int lcta = blockIdx.x - (P.has_stepper ? 1 : 0);
     const int sh = P.my_shard >= 0 ? P.my_shard : lcta % P.n_shards;
     // agents are dealt warp-major across CTAs (of all shards) so every SM
-    // hosts a mix of light and heavy owners: when light agents finish, the
-    // heavy ones on the same SM inherit its FP64 throughput
+    // hosts a mix of light and heavy owners
     const ShardView sv = P.shard[sh];
     bulk_agent<D>(P, *A, warp * P.n_agent_ctas + P.agent_cta_base + lcta, lane, sv);
   }

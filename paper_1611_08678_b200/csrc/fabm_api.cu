@@ -153,6 +153,23 @@ EngineLaunch pick_engine(int sys, int dim) {
 
 int stride_of(int dim) { return dim == 1 ? 1 : (dim == 2 ? 2 : 4); }
 
+// bulk-unit geometry, host side of engine.cuh's seg_class / unit_base
+int host_seg_class(int n) {
+  int lg = 0;
+  while ((2 << lg) <= n) ++lg;  // floor(log2 n)
+  return std::max(0, lg - 4);
+}
+long long host_seg_prefix(long long m, int S) {
+  const long long q = m / S, r = m % S;
+  return static_cast<long long>(S) * q * (q + 1) / 2 + r * (q + 1);
+}
+long long host_unit_base(int J) {
+  const int n = J - kL + 1;
+  const int k = host_seg_class(n), S = 1 << k;
+  const long long lo = k == 0 ? 1 : 1LL << (k + 4);
+  return class_base(k) + host_seg_prefix(n - 1, S) - host_seg_prefix(lo - 1, S);
+}
+
 }  // namespace
 
 static unsigned long long g_last_prof[8];
@@ -193,7 +210,12 @@ struct fabm_plan {
   // IPC handle exposes it to the peer GPUs of a sharded run (config 5)
   char* arena = nullptr;
   size_t arena_bytes = 0;
+  size_t shard_bytes = 0;      // the per-shard prefix {ctrl, ready, F, BK}; the rest is rank 0's unit state
   size_t off_ready = 0, off_F = 0, off_BK = 0;
+  size_t off_claim = 0, off_tdone = 0, off_tstage = 0, off_col = 0, off_PK = 0;
+  int k_max = 0;               // highest segment class (engine.cuh: units)
+  long long n_units = 0;
+  int bulk_default = 0;        // bulk CTAs chosen at creation (fabm_plan_set_bulk_ctas overrides)
   double* F = nullptr;
   double* BK = nullptr;
   int* ready = nullptr;
@@ -283,6 +305,7 @@ fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid_i
     int ctas = (n_targets + kWarps - 1) / kWarps;
     ctas = std::min(ctas, p->num_sms - 1);
     p->bulk_ctas = std::max(ctas, 1);
+    p->bulk_default = p->bulk_ctas;
     const int n_agents = p->bulk_ctas * kWarps;
     if ((n_targets + n_agents - 1) / n_agents > kMaxOwn) {
       set_status(status, FABM_ERR_CONFIG, "n_steps=%lld exceeds the engine capacity", p->N);
@@ -306,7 +329,17 @@ fabm_plan* fabm_plan_create(const fabm_problem* problem, const fabm_grid* grid_i
     p->off_ready = up(sizeof(DevCtrl));
     p->off_F = p->off_ready + up(sizeof(int) * (p->nb + 1));
     p->off_BK = p->off_F + up(sizeof(double) * fl);
-    p->arena_bytes = p->off_BK + up(sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds);
+    p->shard_bytes = p->off_BK + up(sizeof(double) * static_cast<size_t>(p->nb) * kB * 2 * p->ds);
+    // bulk units (engine.cuh): segment classes, unit counts
+    const int nt = std::max(p->nb - kL, 0);
+    p->k_max = nt > 0 ? host_seg_class(nt) : 0;
+    p->n_units = nt > 0 ? host_unit_base(p->nb) : 0;
+    p->off_claim = p->shard_bytes;
+    p->off_tdone = p->off_claim + up(sizeof(int) * static_cast<size_t>(p->n_units + 1));
+    p->off_tstage = p->off_tdone + up(sizeof(int) * (p->nb + 1));
+    p->off_col = p->off_tstage + up(sizeof(int) * (p->nb + 1));
+    p->off_PK = p->off_col + up(sizeof(int) * kMaxClasses * 32);
+    p->arena_bytes = p->off_PK + up(sizeof(double) * static_cast<size_t>(p->n_units) * 32 * 8 * problem->dim);
   }
   if ((e = cudaMalloc(&p->arena, p->arena_bytes)) != cudaSuccess) return fail("malloc arena", e);
   if ((e = cudaMalloc(&p->shard_tab, sizeof(ShardView) * kMaxShards)) != cudaSuccess) return fail("malloc shards", e);
@@ -431,6 +464,18 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     P.shard = p->shard_tab;
   }
   int grid = 1 + p->bulk_ctas;
+  P.has_stepper = 1;
+  {
+    // the bulk units' shared state lives in shard 0's arena (peer memory on
+    // the other GPUs of a sharded run)
+    char* base0 = p->peer[0];
+    P.k_max = p->k_max;
+    P.claim = reinterpret_cast<int*>(base0 + p->off_claim);
+    P.tdone = reinterpret_cast<int*>(base0 + p->off_tdone);
+    P.tstage = reinterpret_cast<int*>(base0 + p->off_tstage);
+    P.col_next = reinterpret_cast<int*>(base0 + p->off_col);
+    P.PK = reinterpret_cast<double*>(base0 + p->off_PK);
+  }
   if (real_shards) {
     // completed targets land in shard 0's accumulators; the stepper lives there
     P.BK = reinterpret_cast<double*>(p->peer[0] + p->off_BK);
@@ -438,7 +483,8 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     P.my_shard = p->rank;
     P.agent_cta_base = p->rank * p->agent_ctas_per_shard;
     P.n_agent_ctas = p->n_shards * p->agent_ctas_per_shard;
-    grid = 1 + p->agent_ctas_per_shard;
+    P.has_stepper = p->rank == 0;
+    grid = (p->rank == 0 ? 1 : 0) + p->agent_ctas_per_shard;
   } else {
     P.my_shard = p->virt ? -1 : 0;
     P.agent_cta_base = 0;
@@ -456,6 +502,9 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
 #endif
   const double tmo = timeout_s > 0 ? timeout_s : 60.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  // dev switches (tools/solo_probe.py, the watchdog test): bits 1, 2 and 8
+  // invalidate the trajectory, so a run that completes with one of them set
+  // reports FABM_ERR_CONFIG instead of FABM_OK
   if (const char* dbg = getenv("FABM_DEBUG_MODE")) P.debug = atoi(dbg);
   CUDA_TRY(cudaEventRecord(p->ev[0], p->stream));
   CUDA_TRY(p->launch(P, grid, p->stream));
@@ -470,6 +519,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
       DevCtrl v{};
       CUDA_TRY(cudaMemcpy(&v, p->peer[sh], sizeof(DevCtrl), cudaMemcpyDeviceToHost));
       h.bulk_tiles += v.bulk_tiles;
+      h.bulk_claims += v.bulk_claims;
       if (h.err_code == ERR_OK && v.err_code != ERR_OK) {
         h.err_code = v.err_code;
         h.err_kind = v.err_kind;
@@ -486,6 +536,8 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   p->stats.steps = p->N;
   p->stats.history_fma = static_cast<int64_t>(p->prob.dim) * p->N * p->N;
   p->stats.bulk_tiles = static_cast<int64_t>(h.bulk_tiles);
+  p->stats.bulk_claims = static_cast<int64_t>(h.bulk_claims);
+  p->stats.segment = 1 << p->k_max;
   p->stats.leader_wait_ns = static_cast<int64_t>(h.leader_wait_ns);
   p->stats.leader_throttle_ns = static_cast<int64_t>(h.leader_throttle_ns);
   for (int i = 0; i < 8; ++i) g_last_prof[i] = h.prof[i];
@@ -504,6 +556,34 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     }
     return h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;
   }
+  if (P.debug & (1 | 2 | 8)) {
+    set_status(status, FABM_ERR_CONFIG, "FABM_DEBUG_MODE=%d: dev switches invalidate the trajectory", P.debug);
+    return FABM_ERR_CONFIG;
+  }
+  return FABM_OK;
+}
+
+int fabm_plan_set_bulk_ctas(fabm_plan* p, int n_ctas, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if (p->n_shards > 1) {
+    set_status(status, FABM_ERR_CONFIG, "set the bulk CTA count before sharding the plan");
+    return FABM_ERR_CONFIG;
+  }
+  const int n_targets = p->nb - kL;
+  int want = n_ctas <= 0 ? p->bulk_default : n_ctas;
+  if (want > p->num_sms - 1 || want < 1) {
+    set_status(status, FABM_ERR_CONFIG, "bulk CTAs must lie in [1, %d], got %d", p->num_sms - 1, n_ctas);
+    return FABM_ERR_CONFIG;
+  }
+  if (n_targets > 0 && (n_targets + want * kWarps - 1) / (want * kWarps) > kMaxOwn) {
+    set_status(status, FABM_ERR_CONFIG, "%d bulk CTAs cannot own %d target blocks (at most %d per agent)", want,
+               n_targets, kMaxOwn);
+    return FABM_ERR_CONFIG;
+  }
+  p->bulk_ctas = want;
+  p->agent_ctas_per_shard = want;
+  p->stats.bulk_ctas = want;
   return FABM_OK;
 }
 
@@ -513,6 +593,8 @@ int fabm_plan_reset(fabm_plan* p, fabm_status* status) {
   CUDA_TRY(cudaSetDevice(p->device));
   CUDA_TRY(cudaMemsetAsync(p->ctrl, 0, sizeof(DevCtrl), p->stream));
   CUDA_TRY(cudaMemsetAsync(p->ready, 0, sizeof(int) * (p->nb + 1), p->stream));
+  // claim words, finished-unit and stage-2 counts, cursors (contiguous)
+  CUDA_TRY(cudaMemsetAsync(p->arena + p->off_claim, 0, p->off_PK - p->off_claim, p->stream));
   for (char* va : p->virt_arenas) CUDA_TRY(cudaMemsetAsync(va, 0, sizeof(DevCtrl), p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   p->armed = true;
@@ -540,8 +622,8 @@ int fabm_plan_set_virtual_shards(fabm_plan* p, int n_shards, fabm_status* status
   p->peer.assign(1, p->arena);
   for (int sh = 1; sh < n_shards; ++sh) {
     char* m = nullptr;
-    CUDA_TRY(cudaMalloc(&m, p->arena_bytes));
-    CUDA_TRY(cudaMemsetAsync(m, 0, p->arena_bytes, p->stream));
+    CUDA_TRY(cudaMalloc(&m, p->shard_bytes));
+    CUDA_TRY(cudaMemsetAsync(m, 0, p->shard_bytes, p->stream));
     p->virt_arenas.push_back(m);
     p->peer.push_back(m);
   }

@@ -12,8 +12,10 @@ Two sharded paths:
   over NVLink (f rows out of rank 0, finished target-block sums into rank 0).
   This replaces the reference's block-partitioned ParallelABM
   (parallel/block.py:44-236), whose lower workers send per-step partial sums
-  to the owner; here each future block costs one store, and the result is
-  bitwise equal to the single-GPU solve.
+  to the owner: here the history of each target block is cut into fixed
+  segments whose partial sums any GPU may compute, and rank 0 adds them once
+  per target block in a fixed order -- one reduction per future block, not
+  per step -- so the result is bitwise equal to the single-GPU solve.
 """
 
 from __future__ import annotations
@@ -69,24 +71,60 @@ def gather_rows(local: np.ndarray, count: int, world: int, rank: int, group=None
 def solve_batch_distributed(problems, grid, *, solver=None, device: int | None = None, group=None):
     """Shard a sweep over the ranks of the default process group.
 
-    Returns (y_last of the whole sweep on every rank, this rank's BatchResult).
-    `solver` defaults to :func:`paper_1611_08678_b200.solve_batch_gpu`.
+    Returns (y_last of the whole sweep on every rank, this rank's BatchResult
+    or None for an empty slice).  `solver` defaults to
+    :func:`paper_1611_08678_b200.solve_batch_gpu`.  Collective: every rank
+    reaches the gather even when its own slice is empty or its solve fails;
+    a failure anywhere raises the same exception on every rank (the lowest
+    failing trajectory of the sweep for a non-finite rhs, with its global
+    ``index``), so no rank is left blocked in the collective.
     """
     import torch.distributed as dist
 
     if solver is None:
         from .solver import solve_batch_gpu as solver
     problems = list(problems)
+    if not problems:
+        raise ValueError("solve_batch_distributed needs at least one problem")
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     lo, hi = shard_bounds(len(problems), world, rank)
-    kwargs = {"states": False}
+    kwargs = {"states": False, "raise_on_error": False}
     if device is None and "LOCAL_RANK" in os.environ:
         device = int(os.environ["LOCAL_RANK"])  # one process per GPU (torchrun)
     if device is not None:
         kwargs["device"] = device
-    res = solver(problems[lo:hi], grid, **kwargs)
-    return gather_rows(res.y_last, len(problems), world, rank, group), res
+    res, err = None, None
+    d = int(problems[0].dim)
+    local = np.zeros((hi - lo, d))
+    if hi > lo:
+        try:
+            res = solver(problems[lo:hi], grid, **kwargs)
+            local = np.asarray(res.y_last, dtype=np.float64).reshape(hi - lo, d)
+            if getattr(res, "error", None) is not None:
+                idx, exc = res.error
+                exc.index = lo + int(idx)
+                err = exc
+        except Exception as exc:  # keep the collective sequence aligned across ranks
+            err = exc
+    rec = _error_record(err)
+    if rec is not None and rec[0] == "step":
+        rec = rec + (getattr(err, "index", None),)
+    if world > 1:
+        records = [None] * world
+        dist.all_gather_object(records, rec, group=group)
+    else:
+        records = [rec]
+    bad = [(r, x) for r, x in enumerate(records) if x is not None]
+    if bad:
+        # the lowest failing trajectory of the sweep (ranks hold ascending slices)
+        r, x = bad[0]
+        if x[0] == "step":
+            exc = _raise_record_exc(x[:4], r)
+            exc.index = x[4]
+            raise exc
+        _raise_record(x[:4], r)
+    return gather_rows(local, len(problems), world, rank, group), res
 
 
 def _error_record(exc):
@@ -105,17 +143,21 @@ def _error_record(exc):
     return ("runtime", f"{type(exc).__name__}: {exc}", None, None)
 
 
-def _raise_record(rec, rank):
+def _raise_record_exc(rec, rank):
     from .core import SolverStepError, StrategyTimeoutError
 
     kind, msg, step, t = rec
     if kind == "step":
-        raise SolverStepError("rhs returned a non-finite value", step=step, t=t)
+        return SolverStepError("rhs returned a non-finite value", step=step, t=t)
     if kind == "timeout":
-        raise StrategyTimeoutError(f"rank {rank}: {msg}")
+        return StrategyTimeoutError(f"rank {rank}: {msg}")
     if kind == "value":
-        raise ValueError(msg)
-    raise RuntimeError(f"rank {rank}: {msg}")
+        return ValueError(msg)
+    return RuntimeError(f"rank {rank}: {msg}")
+
+
+def _raise_record(rec, rank):
+    raise _raise_record_exc(rec, rank)
 
 
 def first_error(records):
@@ -131,7 +173,7 @@ def first_error(records):
 
 
 def solve_sharded(problem, grid, *, weights="accurate", device: int | None = None, timeout_s: float | None = None,
-                  group=None, plan_cls=None):
+                  group=None, plan_cls=None, stats: dict | None = None):
     """Integrate ONE trajectory with its history sharded over the ranks of
     ``group`` (one process per GPU).  Collective: every rank calls it with the
     same problem and grid.  Rank 0 returns the :class:`Trajectory`, the others
@@ -149,7 +191,7 @@ def solve_sharded(problem, grid, *, weights="accurate", device: int | None = Non
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", rank))
     if world == 1 and plan_cls is None:
-        return solve_gpu(problem, grid, weights=weights, device=device, timeout_s=timeout_s)
+        return solve_gpu(problem, grid, weights=weights, device=device, timeout_s=timeout_s, stats=stats)
     if plan_cls is None:
         plan_cls = GpuPlan
     if not grid.spans(problem.t_end):
@@ -180,6 +222,8 @@ def solve_sharded(problem, grid, *, weights="accurate", device: int | None = Non
     if err is None:
         try:
             plan.run(timeout_s)
+            if stats is not None:
+                stats.update(plan.stats())  # this rank's engine counters (kernel_ms: its own launch)
         except Exception as exc:
             err = exc
     records = [None] * world

@@ -112,6 +112,17 @@ def _weight_arrays(weights, alpha: float, n_steps: int):
     return nat.WEIGHTS_HOST, arrs
 
 
+def _weights_key(weights, alpha: float, n_steps: int):
+    """Identity of the table ``weights`` resolves to, or None if unknown (a
+    caller's table object may be mutated between calls: always re-upload)."""
+    if not isinstance(weights, str):
+        return None
+    if weights == "reference":
+        # the seam: a monkeypatched precompute_weights is a different table
+        return ("reference", precompute_weights, alpha, n_steps)
+    return (weights, alpha, n_steps)
+
+
 class GpuPlan:
     """Device-resident buffers for one (problem, grid) on one GPU.
 
@@ -136,6 +147,13 @@ class GpuPlan:
 
     # -- configuration -------------------------------------------------
     def set_weights(self, weights):
+        # the device table only changes with its inputs: a plan re-used for the
+        # same (mode or table source, alpha, N) keeps it (no host table, no
+        # upload, no regeneration)
+        key = _weights_key(weights, float(self.problem.alpha), int(self.grid.n_steps))
+        if key is not None and key == getattr(self, "_weights_key", None):
+            return
+        self._weights_key = None
         mode, arrs = _weight_arrays(weights, float(self.problem.alpha), int(self.grid.n_steps))
         st = nat.Status()
         ptrs = [nat.dptr(a) for a in arrs] if arrs else [None, None, None]
@@ -143,11 +161,20 @@ class GpuPlan:
         if rc != nat.FABM_OK:
             _raise_status(st)
         self.weights_mode = weights if isinstance(weights, str) else "table"
+        self._weights_key = key
 
     def set_y0(self, y0):
         y0 = np.ascontiguousarray(np.asarray(y0, dtype=np.float64).reshape(-1))
         st = nat.Status()
         if self._lib.fabm_plan_set_y0(self._h, nat.dptr(y0), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    def set_bulk_ctas(self, n_ctas: int | None):
+        """Cap the CTAs that run bulk agents (None: one per SM besides the
+        stepper).  The result does not depend on it: the bulk units and the
+        reduction order are fixed by n_steps."""
+        st = nat.Status()
+        if self._lib.fabm_plan_set_bulk_ctas(self._h, int(n_ctas or 0), ctypes_ref(st)) != nat.FABM_OK:
             _raise_status(st)
 
     # -- sharding (config 5, DESIGN.md §4) ------------------------------
@@ -349,6 +376,7 @@ def _cached_plan(problem, grid, weights, device) -> GpuPlan:
     if plan is not None and isinstance(weights, str):
         _PLAN_CACHE.move_to_end(key)
         plan.problem = problem
+        plan.set_weights(weights)  # a no-op unless the table source changed (e.g. a patched seam)
         return plan
     plan = GpuPlan(problem, grid, weights=weights, device=device)
     if isinstance(weights, str):
@@ -394,12 +422,7 @@ def solve_gpu(
     if int(problem.dim) > nat.MAX_DIM and tag.name in COMPONENTWISE:
         return _solve_by_components(problem, grid, tag, weights=weights, device=device, timeout_s=timeout_s,
                                     stats=stats)
-    cached = _PLAN_CACHE_SIZE and isinstance(weights, str)
     plan = _cached_plan(problem, grid, weights, device)
-    if cached:
-        # a solve owns its weight table, as in the reference (serial.py:130):
-        # regenerate it on reuse (device modes cost ~1 ms at N=1e6)
-        plan.set_weights(weights)
     plan.set_y0(problem.y0)
     traj = plan.run_to_host(timeout_s)
     if stats is not None:

@@ -11,15 +11,14 @@ the reference switch unchanged, and run on the one-launch GPU engine, which
 supersedes both decompositions: the bulk Toeplitz tiles play
 the senders' partial sums, the stepper the owner.  ``n_workers`` and
 ``chunk`` are validated as in the reference; the worker counters in
-``stats`` are zero (no host workers exist) and the engine's own counters are
-added.
+``stats`` are None (no host workers exist: "not applicable") and the
+engine's own counters are added.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
-import numpy as np
 
 from .solver import solve_gpu
 
@@ -68,6 +67,16 @@ def idle_fraction(plan: PartitionPlan, worker: int) -> float:
     return min(worker * plan.block_size, plan.n_steps) / plan.n_steps
 
 
+def _not_applicable(stats: dict) -> None:
+    # the reference's per-worker counters (block.py:230-231, reduction.py:
+    # 348-349) describe host workers that do not exist here: present, None
+    # ("not applicable"), with the engine's own counters beside them
+    stats["idle_steps"] = None
+    stats["partial_sums_sent"] = None
+    stats["worker_counters"] = ("not applicable: no host workers; the engine reports bulk_tiles, "
+                                "bulk_claims, leader_wait_ns instead")
+
+
 def _check_grid(problem, grid):
     N = grid.n_steps
     if not grid.spans(problem.t_end):
@@ -83,8 +92,7 @@ def solve_block_parallel(problem, grid, n_workers: int, *, watchdog_s: float = D
     traj = solve_gpu(problem, grid, weights="reference", device=device, timeout_s=watchdog_s, stats=eng)
     if stats is not None:
         stats.update(eng)
-        stats["idle_steps"] = np.zeros(plan.n_workers, dtype=np.int64)
-        stats["partial_sums_sent"] = np.zeros(plan.n_workers, dtype=np.int64)
+        _not_applicable(stats)
         stats["plan"] = plan
     return traj
 
@@ -104,7 +112,6 @@ def solve_reduction_parallel(problem, grid, n_workers: int, chunk: int = 1024, *
     traj = solve_gpu(problem, grid, weights="reference", device=device, timeout_s=watchdog_s, stats=eng)
     if stats is not None:
         stats.update(eng)
-        stats["idle_steps"] = np.zeros(n_workers, dtype=np.int64)
-        stats["partial_sums_sent"] = np.zeros(n_workers, dtype=np.int64)
+        _not_applicable(stats)
         stats["chunk"] = chunk
     return traj

@@ -32,7 +32,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
-from .core import FractionalProblem, GridSpec
+from .core import FractionalProblem, GridSpec, SolverStepError
 from .solver import GpuPlan, solve_batch_gpu, solve_gpu
 from .systems import rhs_linear, rhs_power_law
 
@@ -195,23 +195,40 @@ def check_power_law_orders(alphas=(0.3, 0.5, 0.8, 1.0), n_list=(500, 1000, 2000)
     return results, reports
 
 
-def check_constant_forcing(alpha: float = 0.5, n_steps: int = 500, *, device: int = 0) -> CheckResult:
-    """beta = alpha: constant forcing, exact solution t^alpha (checks.py:110-126)."""
+def check_constant_forcing(alpha: float = 0.5, n_steps: int = 500, *, weights="reference",
+                           device: int = 0) -> CheckResult:
+    """beta = alpha: constant forcing, exact solution t^alpha (checks.py:103-119).
+
+    ``weights``: the table the solve uses -- by default the reference's
+    ``precompute_weights`` (through :data:`solver.precompute_weights`, the
+    seam of serial.py:24-31), or a mode / table as for :func:`solve_gpu`.  A
+    corrupted table (e.g. ``c = 0``) must fail this check
+    (pkg/tests/test_verify.py:167-180)."""
     problem = _power_problem(alpha, beta=alpha)
     grid = problem.grid(n_steps)
-    traj = solve_gpu(problem, grid, weights="reference", device=device)
+    try:
+        traj = solve_gpu(problem, grid, weights=weights, device=device)
+    except SolverStepError as exc:
+        return CheckResult(f"constant-forcing exactness alpha={alpha:g} [gpu]", False, f"solver failed: {exc}")
     err = float(np.max(np.abs(traj.states[:, 0] - grid.times() ** alpha)))
     return CheckResult(f"constant-forcing exactness alpha={alpha:g} [gpu]", err <= 1e-10,
                        f"sup error {err:.3e} (roundoff expected)")
 
 
 def check_linear_mittag_leffler(n_steps: int = 4000, lam: float = -1.0, alpha: float = 0.5, t_end: float = 1.0,
-                                *, device: int = 0) -> CheckResult:
-    """Terminal value of the linear problem against the device series (checks.py:129-141)."""
+                                *, weights="reference", device: int = 0) -> CheckResult:
+    """Terminal value of the linear problem against the device series
+    (checks.py:122-141).  A table with the predictor sign flipped must fail
+    it (pkg/tests/test_verify.py:151-165)."""
     problem = FractionalProblem(alpha=alpha, dim=1, rhs=rhs_linear(lam), y0=[1.0], t_end=t_end)
-    traj = solve_gpu(problem, problem.grid(n_steps), device=device)
+    try:
+        traj = solve_gpu(problem, problem.grid(n_steps), weights=weights, device=device)
+    except SolverStepError as exc:
+        return CheckResult("linear Mittag-Leffler [gpu]", False, f"solver failed: {exc}")
     exact = mittag_leffler(alpha, lam * t_end ** alpha, device=device)
     err = abs(float(traj.states[-1, 0]) - exact)
+    if not math.isfinite(err):
+        err = math.inf
     return CheckResult("linear Mittag-Leffler [gpu]", err <= ML_TOL,
                        f"|y_N - E_{alpha:g}({lam * t_end ** alpha:g})| = {err:.3e} (tol {ML_TOL:g})")
 
@@ -220,17 +237,57 @@ def _sup_rel_dev(a: np.ndarray, b: np.ndarray) -> float:
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)))
 
 
-def check_strategy_equivalence(n_steps: int = 2048, n_shards: int = 2, *, device: int = 0) -> list[CheckResult]:
-    """The device code paths against each other on the power-law problem (checks.py:144-168).
+def _reference_solve_serial():
+    """The reference's own ``solve_serial`` when the reference package is
+    importable (installed next to this one, e.g. baseline/_ref), else None."""
+    import importlib
+    import sys
+    from pathlib import Path
 
-    The single-trajectory engine is the reference point; the batch engine is
-    an independent kernel (same ACCURATE weights), and the sharded protocol
-    emulation must be bitwise equal to it.
+    try:
+        return importlib.import_module("fodeabm").solve_serial
+    except ImportError:
+        pass
+    ref = Path(__file__).resolve().parents[1] / "baseline" / "_ref"
+    if (ref / "fodeabm").is_dir():
+        sys.path.append(str(ref))
+        try:
+            return importlib.import_module("fodeabm").solve_serial
+        except ImportError:
+            return None
+    return None
+
+
+def check_strategy_equivalence(n_steps: int = 2048, n_shards: int = 2, *, device: int = 0) -> list[CheckResult]:
+    """The device code paths against the serial solver and each other on the
+    power-law problem (checks.py:144-168).
+
+    * ``gpu vs solve_serial``: the engine with the reference's table against
+      the reference's own ``solve_serial`` (its tolerance EQUIV_TOL), when the
+      reference package is importable; the check is reported as not run
+      otherwise (it does not pass silently);
+    * ``step residual``: every step of the engine's trajectory re-evaluated by
+      the independent single-step kernel (``steps.trajectory_residual``);
+    * the batch engine (an independent kernel, same ACCURATE weights) and the
+      sharded-protocol emulation (bitwise) against the engine.
     """
+    from .core import precompute_weights
+    from .steps import trajectory_residual
+
     problem = _power_problem(0.5)
     grid = problem.grid(n_steps)
-    ref = solve_gpu(problem, grid, weights="accurate", device=device)
     out = []
+    serial = _reference_solve_serial()
+    dev_ref = solve_gpu(problem, grid, weights="reference", device=device)
+    if serial is not None:
+        ref_traj = serial(problem, grid)
+        dev = _sup_rel_dev(dev_ref.states, np.asarray(ref_traj.states))
+        out.append(CheckResult("gpu vs solve_serial [gpu]", dev <= EQUIV_TOL, f"sup rel dev {dev:.3e}"))
+    else:
+        out.append(CheckResult("gpu vs solve_serial [gpu]", False, "not run: the reference package is not importable"))
+    res = trajectory_residual(problem, precompute_weights(problem.alpha, n_steps), dev_ref, device=device)
+    out.append(CheckResult("step residual [gpu]", res <= EQUIV_TOL, f"normwise residual {res:.3e}"))
+    ref = solve_gpu(problem, grid, weights="accurate", device=device)
     batch = solve_batch_gpu([problem], grid, states=True, device=device)
     dev = _sup_rel_dev(batch.states[0], ref.states)
     out.append(CheckResult("batch engine [gpu]", dev <= EQUIV_TOL, f"sup rel dev {dev:.3e}"))

@@ -101,4 +101,68 @@ def test_gpu_verification_suite_passes():
     results, reports = run_verification_suite()
     failed = [r for r in results if not r.passed]
     assert not failed, failed
-    assert len(reports) == 4 and len(results) == 4 + 1 + 1 + 2
+    assert len(reports) == 4 and len(results) == 4 + 1 + 1 + 4
+
+
+# ---- mutation detection (pkg/tests/test_verify.py:143-180): the device
+# verification suite must FAIL on a sabotaged weight table, whether it comes
+# through the precompute_weights seam or is passed in directly
+def _sabotaged_flip_b(real):
+    def fn(alpha, n_steps):
+        from paper_1611_08678_b200.core import WeightTable
+
+        table = real(alpha, n_steps)
+        n = np.arange(n_steps + 1, dtype=np.float64)
+        bad_b = ((n + 1.0) ** alpha + n ** alpha) / math.gamma(alpha + 1.0)  # the paper's printed "+"
+        return WeightTable(alpha=alpha, b=bad_b, a=table.a, c=table.c)
+
+    return fn
+
+
+def _sabotaged_zero_c(real):
+    def fn(alpha, n_steps):
+        from paper_1611_08678_b200.core import WeightTable
+
+        table = real(alpha, n_steps)
+        return WeightTable(alpha=alpha, b=table.b, a=table.a, c=np.zeros(n_steps + 1))
+
+    return fn
+
+
+@pytest.mark.gpu
+def test_flipped_predictor_sign_fails_verification(monkeypatch):
+    from paper_1611_08678_b200 import solver, verify
+
+    assert verify.check_linear_mittag_leffler(n_steps=500).passed
+    real = solver.precompute_weights
+    monkeypatch.setattr(solver, "precompute_weights", _sabotaged_flip_b(real))
+    assert not verify.check_linear_mittag_leffler(n_steps=500).passed
+    monkeypatch.undo()
+    # the same table passed explicitly
+    bad = _sabotaged_flip_b(real)(0.5, 500)
+    assert not verify.check_linear_mittag_leffler(n_steps=500, weights=bad).passed
+    assert verify.check_linear_mittag_leffler(n_steps=500).passed  # the seam is restored
+
+
+@pytest.mark.gpu
+def test_missing_first_node_term_fails_verification(monkeypatch):
+    from paper_1611_08678_b200 import solver, verify
+
+    assert verify.check_constant_forcing(n_steps=500).passed
+    real = solver.precompute_weights
+    monkeypatch.setattr(solver, "precompute_weights", _sabotaged_zero_c(real))
+    assert not verify.check_constant_forcing(n_steps=500).passed
+    monkeypatch.undo()
+    bad = _sabotaged_zero_c(real)(0.5, 500)
+    assert not verify.check_constant_forcing(n_steps=500, weights=bad).passed
+
+
+@pytest.mark.gpu
+def test_strategy_equivalence_includes_serial_oracle_row():
+    from paper_1611_08678_b200 import verify
+
+    rows = {r.name: r for r in verify.check_strategy_equivalence()}
+    assert "gpu vs solve_serial [gpu]" in rows and "step residual [gpu]" in rows
+    assert rows["step residual [gpu]"].passed, rows["step residual [gpu]"].detail
+    # baseline/_ref travels with the repo to the GPU box: the reference is importable there
+    assert rows["gpu vs solve_serial [gpu]"].passed, rows["gpu vs solve_serial [gpu]"].detail

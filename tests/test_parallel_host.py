@@ -33,7 +33,34 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+class FakeProblem:
+    def __init__(self, alpha, idx):
+        self.alpha, self.idx, self.dim = alpha, idx, 2
+
+
+class FakeResult:
+    def __init__(self, y, error=None):
+        self.y_last = y
+        self.error = error
+
+
+def _fake_solver(problems, grid, **kw):
+    # a stand-in for solve_batch_gpu: y_N = (alpha, index) per member; the
+    # member with idx == grid["fail"] has a non-finite rhs (raise_on_error
+    # False: reported, not raised), idx == grid["crash"] raises outright
+    from paper_1611_08678_b200.core import SolverStepError
+
+    assert kw.get("raise_on_error") is False
+    err = None
+    for i, p in enumerate(problems):
+        if grid and p.idx == grid.get("crash"):
+            raise RuntimeError("device lost")
+        if grid and p.idx == grid.get("fail") and err is None:
+            err = (i, SolverStepError("rhs returned a non-finite value", step=17, t=0.018))
+    return FakeResult(np.array([[p.alpha, p.idx] for p in problems], dtype=np.float64), err)
+
+
+def _worker(rank, world, port, q, count, grid):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -42,35 +69,55 @@ def _worker(rank, world, port, q):
     try:
         from paper_1611_08678_b200.parallel import solve_batch_distributed
 
-        class FakeResult:
-            def __init__(self, y):
-                self.y_last = y
-
-        def fake_solver(problems, grid, **kw):
-            # a stand-in for solve_batch_gpu: y_N = (alpha, index) per member
-            return FakeResult(np.array([[p[0], p[1]] for p in problems], dtype=np.float64))
-
-        problems = [(0.9 + 0.1 * i / 7, float(i)) for i in range(7)]
-        y_all, _ = solve_batch_distributed(problems, None, solver=fake_solver)
-        q.put((rank, y_all.tolist()))
+        problems = [FakeProblem(0.9 + 0.1 * i / 7, float(i)) for i in range(count)]
+        try:
+            y_all, _ = solve_batch_distributed(problems, grid, solver=_fake_solver)
+            q.put((rank, ("ok", y_all.tolist())))
+        except Exception as exc:  # noqa: BLE001
+            q.put((rank, ("raised", type(exc).__name__, getattr(exc, "step", None), getattr(exc, "index", None))))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_sweep_gathers_in_order_gloo():
+def _run_world2(count, grid=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, count, grid)) for r in range(2)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return results
+
+
+def test_sharded_sweep_gathers_in_order_gloo():
+    results = _run_world2(7)
     want = [[0.9 + 0.1 * i / 7, float(i)] for i in range(7)]
     for rank in (0, 1):
-        np.testing.assert_allclose(results[rank], want)
+        assert results[rank][0] == "ok"
+        np.testing.assert_allclose(results[rank][1], want)
+
+
+def test_sharded_sweep_empty_slice_does_not_hang_gloo():
+    # one trajectory over two ranks: rank 1's slice is empty
+    results = _run_world2(1)
+    for rank in (0, 1):
+        assert results[rank] == ("ok", [[0.9, 0.0]])
+
+
+def test_sharded_sweep_error_raised_on_every_rank_gloo():
+    # member 5 (rank 1's slice) has a non-finite rhs: both ranks raise the
+    # same SolverStepError, with the global index of the failing member
+    results = _run_world2(7, {"fail": 5.0})
+    for rank in (0, 1):
+        assert results[rank] == ("raised", "SolverStepError", 17, 5)
+    # a solver crash on rank 0 does not leave rank 1 blocked in the gather
+    results = _run_world2(7, {"crash": 1.0})
+    for rank in (0, 1):
+        assert results[rank][:2] == ("raised", "RuntimeError")
 
 
 def test_gather_rows_single_process_identity():

@@ -31,7 +31,7 @@ for arg in sys.argv[1:] or ["100000"]:
     print(f"N={N:.0e} {ms:9.3f} ms  {N / (ms * 1e-3):.4e} steps/s  wait={st['leader_wait_ns'] / 1e6:.1f} ms  "
           f"throttle={st['leader_throttle_ns'] / 1e6:.1f} ms  leader={buf[0] / N:.1f} cyc/step  fast={buf[1] * 8 / N:.3f}  "
           f"lag={buf[2] * 8 / N:.1f}  helper1 wait={buf[3] / N:.0f} proc={buf[7] / N:.0f} cyc/step  "
-          f"yN={plan.last_state().tolist()}", flush=True)
+          f"seg={st.get('segment')} claims={st.get('bulk_claims')} yN={plan.last_state().tolist()}", flush=True)
     plan.close()
     if os.environ.get("FABM_SOLO"):
         os.environ["FABM_DEBUG_MODE"] = "1"
