@@ -333,7 +333,9 @@ def reference_parallel_sample(n_target: int) -> dict | None:
         h = T_END / N_STEPS
         for name, fn in (("block", fodeabm.solve_block_parallel), ("reduction", fodeabm.solve_reduction_parallel)):
             samples = []
-            for m in (20000, 40000):
+            # prefixes long enough for the O(M^2) history term to show beside
+            # the per-step synchronisation of the workers
+            for m in (100000, 200000):
                 prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
                 t0 = time.perf_counter()
                 fn(prob, fodeabm.GridSpec(n_steps=m, h=h), P)
@@ -341,6 +343,8 @@ def reference_parallel_sample(n_target: int) -> dict | None:
             (m1, t1), (m2, t2) = samples
             c = (t2 / m2 - t1 / m1) / (m2 - m1)
             a = max(t1 / m1 - c * m1, 0.0)
+            if c <= 0:  # per-step overheads dominate both prefixes: a quadratic through the longer one
+                c, a = t2 / (m2 * m2), 0.0
             t_full = a * n_target + c * n_target * n_target
             out[name] = {"value": n_target / t_full, "unit": UNIT, "cores": P, "kind": "reference", "projected": True,
                          "sample": (f"fodeabm.solve_{name}_parallel (baseline/_ref, unmodified) P={P} workers, "

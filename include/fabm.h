@@ -203,6 +203,18 @@ int fabm_plan_attach_shards(fabm_plan* plan, int n_shards, int rank, const void*
 /* Close the peer mappings (every rank, then barrier, then destroy: an arena
  * must outlive the peers' mappings of it). */
 int fabm_plan_detach_shards(fabm_plan* plan, fabm_status* status);
+/* On rank 0 of an attached plan: run every shard's agents in THIS launch
+ * (as fabm_plan_set_virtual_shards does), with the peers' arenas -- their f
+ * copies and control blocks -- used through their CUDA IPC mappings.  Only
+ * rank 0 launches, so no kernels on different launches wait on each other:
+ * the cross-process IPC path (handle export, open, system-scope flags and
+ * stores into a peer's memory, detach) runs where only one GPU is available
+ * (tests/test_gpu_sharded_ipc.py).  on = 0 restores the per-rank launches. */
+int fabm_plan_emulate_shards(fabm_plan* plan, int on, fabm_status* status);
+/* This plan's own control block after a run: source blocks released into it
+ * (src_done) and Toeplitz tiles its shard's agents processed. */
+int fabm_plan_shard_counters(const fabm_plan* plan, int64_t* src_done, int64_t* bulk_tiles,
+                             fabm_status* status);
 /* One-GPU emulation of an n-shard run: separate per-shard f copies, control
  * blocks and scratch on this device, agent CTA b serving shard (b-1) % n.
  * Exercises the sharded protocol where only one GPU is available. */

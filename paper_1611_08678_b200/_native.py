@@ -55,6 +55,8 @@ EXPORTED_SYMBOLS = (
     "fabm_plan_ipc_handle",
     "fabm_plan_attach_shards",
     "fabm_plan_set_virtual_shards",
+    "fabm_plan_emulate_shards",
+    "fabm_plan_shard_counters",
     "fabm_plan_detach_shards",
     "fabm_solve_batch",
     "fabm_measure_dfma_peak",
@@ -149,6 +151,8 @@ def _declare(lib):
         "fabm_plan_ipc_handle": (ctypes.c_int, [plan, ctypes.c_void_p, S]),
         "fabm_plan_attach_shards": (ctypes.c_int, [plan, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, S]),
         "fabm_plan_set_virtual_shards": (ctypes.c_int, [plan, ctypes.c_int, S]),
+        "fabm_plan_emulate_shards": (ctypes.c_int, [plan, ctypes.c_int, S]),
+        "fabm_plan_shard_counters": (ctypes.c_int, [plan, _I64P, _I64P, S]),
         "fabm_plan_detach_shards": (ctypes.c_int, [plan, S]),
         "fabm_solve_batch": (ctypes.c_int, [P, G, ctypes.c_int64, ctypes.c_int, _DP, _DP, _DP, _DP, S]),
         "fabm_measure_dfma_peak": (ctypes.c_double, [ctypes.c_int]),

@@ -896,6 +896,14 @@ constexpr int kMaxClasses = 32;
 #define FABM_DYN_BURST 4
 #endif
 constexpr int kDynBurst = FABM_DYN_BURST;  // chunks of a claimed unit between selections
+#ifndef FABM_OWN_BATCH
+#define FABM_OWN_BATCH 1
+#endif
+#ifndef FABM_URGENT
+#define FABM_URGENT 16
+#endif
+constexpr int kOwnBatch = FABM_OWN_BATCH;  // frontier chunks taken together (unless urgent)
+constexpr int kUrgent = FABM_URGENT;       // blocks before a target's deadline that make any chunk urgent
 __device__ __forceinline__ int seg_class(int n) {
   const int k = 31 - __clz(n) - 4;
   return k > 0 ? k : 0;
@@ -1080,22 +1088,34 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       last_progress = global_ns();
     }
     __syncwarp();
-    // earliest owned target with a published chunk in its current unit
-    int best = -1;
+    // earliest owned target with published chunks in its current unit.
+    // ELIGIBLE: a batch of >= kOwnBatch chunks, the rest of its unit, or a
+    // deadline within kUrgent blocks -- single frontier chunks of distant
+    // targets wait and are taken in batches (fewer spill/reload switches);
+    // PENDING (any published chunk) is the fallback before idling
+    int best = -1, any = -1;
     for (int b0 = 0; b0 < nown; b0 += 32) {
       const int i = b0 + lane;
-      bool pend = false;
+      bool pend = false, elig = false;
       if (i < nown) {
-        const int n = owned_target(agent, i, nA) - kL + 1;
+        const int J = owned_target(agent, i, nA);
+        const int n = J - kL + 1;
         const int S = 1 << seg_class(n);
         const int nx = A.own_next[i] >> 1;
         const int uhi = min((nx / S + 1) * S, n);
-        pend = nx < min(uhi, M);
+        const int avail = min(uhi, M) - nx;
+        pend = avail > 0;
+        elig = pend && (avail >= kOwnBatch || uhi <= M || J - M <= kUrgent);
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, pend);
-      if (bal) { best = b0 + __ffs(bal) - 1; break; }
+      const unsigned balp = __ballot_sync(0xffffffffu, pend);
+      const unsigned bale = __ballot_sync(0xffffffffu, elig);
+      if (any < 0 && balp) any = b0 + __ffs(balp) - 1;
+      if (bale) { best = b0 + __ffs(bale) - 1; break; }
     }
     const int Jo = best >= 0 ? owned_target(agent, best, nA) : 0x7fffffff;
+    // nearest deadline among this agent's owned targets (a claimed-unit burst
+    // yields to it once it is within kUrgent blocks)
+    const int j_soon = any >= 0 ? owned_target(agent, any, nA) : 0x7fffffff;
     // earliest claimable unit; the cursors only grow, so a bound read at
     // the same M stays a lower bound
     int Jd = 0x7fffffff, kd = 0, cd = -1;
@@ -1109,6 +1129,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       lb_M = M;
     }
     const bool take_dyn = Jd < Jo;
+    if (!take_dyn && best < 0) best = any;  // nothing eligible or claimable: a lone pending chunk
     if (!take_dyn && best < 0) {
       // nothing to do: finished, or wait for the next source block
       bool fin = dJ < 0 && kc > P.k_max;
@@ -1165,7 +1186,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       hi = min((s + 1) << seg_class(J - kL + 1), J - kL + 1);
       lim = hi;  // a complete column: every chunk is published
     } else {
-      J = Jo;
+      J = owned_target(agent, best, nA);
       const int n = J - kL + 1;
       const int S = 1 << seg_class(n);
       const int v = A.own_next[best];
@@ -1207,7 +1228,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
-      if (!take_dyn && M2 != M) break;  // a newer source block arrived: re-run the selection
+      if (M2 != M && (!take_dyn || j_soon - M2 <= kUrgent)) break;  // a newer source block: re-run the selection
     }
     APROF(c_tile)
     __syncwarp();

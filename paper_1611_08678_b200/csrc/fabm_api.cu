@@ -225,6 +225,7 @@ struct fabm_plan {
   int n_shards = 1;
   int rank = 0;
   bool virt = false;
+  bool emulate = false;        // attached peers, but one launch here serves every shard (fabm_plan_emulate_shards)
   bool armed = false;          // real sharded runs: flags reset and not yet run
   int agent_ctas_per_shard = 0;
   std::vector<char*> peer;     // arena base of every shard (peer[rank] = arena)
@@ -421,7 +422,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     int rc = fabm_plan_set_weights(p, FABM_WEIGHTS_ACCURATE, nullptr, nullptr, nullptr, status);
     if (rc != FABM_OK) return rc;
   }
-  const bool real_shards = p->n_shards > 1 && !p->virt;
+  const bool real_shards = p->n_shards > 1 && !p->virt && !p->emulate;
   if (real_shards) {
     if (!p->armed) {
       set_status(status, FABM_ERR_CONFIG, "sharded plan: call fabm_plan_reset on every rank, then barrier, then run");
@@ -486,7 +487,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     P.has_stepper = p->rank == 0;
     grid = (p->rank == 0 ? 1 : 0) + p->agent_ctas_per_shard;
   } else {
-    P.my_shard = p->virt ? -1 : 0;
+    P.my_shard = (p->virt || p->emulate) ? -1 : 0;
     P.agent_cta_base = 0;
     P.n_agent_ctas = p->bulk_ctas;
   }
@@ -514,7 +515,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   cudaEventElapsedTime(&ms, p->ev[0], p->ev[1]);
   DevCtrl h{};
   CUDA_TRY(cudaMemcpy(&h, p->ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost));
-  if (p->virt) {  // emulated shards: their agents count tiles / raise errors in their own blocks
+  if (p->virt || p->emulate) {  // emulated shards: their agents count tiles / raise errors in their own blocks
     for (int sh = 1; sh < p->n_shards; ++sh) {
       DevCtrl v{};
       CUDA_TRY(cudaMemcpy(&v, p->peer[sh], sizeof(DevCtrl), cudaMemcpyDeviceToHost));
@@ -596,6 +597,8 @@ int fabm_plan_reset(fabm_plan* p, fabm_status* status) {
   // claim words, finished-unit and stage-2 counts, cursors (contiguous)
   CUDA_TRY(cudaMemsetAsync(p->arena + p->off_claim, 0, p->off_PK - p->off_claim, p->stream));
   for (char* va : p->virt_arenas) CUDA_TRY(cudaMemsetAsync(va, 0, sizeof(DevCtrl), p->stream));
+  if (p->emulate)  // the peers' control blocks (IPC mappings) belong to this launch too
+    for (int sh = 1; sh < p->n_shards; ++sh) CUDA_TRY(cudaMemsetAsync(p->peer[sh], 0, sizeof(DevCtrl), p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   p->armed = true;
   return FABM_OK;
@@ -679,6 +682,35 @@ int fabm_plan_attach_shards(fabm_plan* p, int n_shards, int rank, const void* ha
   return FABM_OK;
 }
 
+int fabm_plan_emulate_shards(fabm_plan* p, int on, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  if (on && (p->n_shards < 2 || p->virt || p->rank != 0)) {
+    set_status(status, FABM_ERR_CONFIG, "emulate: needs a plan attached to peer shards, on rank 0");
+    return FABM_ERR_CONFIG;
+  }
+  p->emulate = on != 0;
+  if (p->emulate) {
+    p->agent_ctas_per_shard = p->bulk_ctas;
+    p->stats.bulk_ctas = p->bulk_ctas;
+  } else if (p->n_shards > 1) {
+    p->agent_ctas_per_shard = shard_ctas(p, p->n_shards);
+    p->stats.bulk_ctas = p->agent_ctas_per_shard;
+  }
+  return FABM_OK;
+}
+
+int fabm_plan_shard_counters(const fabm_plan* p, int64_t* src_done, int64_t* bulk_tiles, fabm_status* status) {
+  clear_status(status);
+  if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
+  CUDA_TRY(cudaSetDevice(p->device));
+  DevCtrl h{};
+  CUDA_TRY(cudaMemcpy(&h, p->ctrl, sizeof(DevCtrl), cudaMemcpyDeviceToHost));
+  if (src_done) *src_done = h.src_done;
+  if (bulk_tiles) *bulk_tiles = static_cast<int64_t>(h.bulk_tiles);
+  return FABM_OK;
+}
+
 int fabm_plan_detach_shards(fabm_plan* p, fabm_status* status) {
   clear_status(status);
   if (!p) { set_status(status, FABM_ERR_CONFIG, "null plan"); return FABM_ERR_CONFIG; }
@@ -692,6 +724,7 @@ int fabm_plan_detach_shards(fabm_plan* p, fabm_status* status) {
   p->n_shards = 1;
   p->rank = 0;
   p->virt = false;
+  p->emulate = false;
   p->armed = false;
   p->agent_ctas_per_shard = p->bulk_ctas;
   p->stats.bulk_ctas = p->bulk_ctas;

@@ -200,6 +200,22 @@ class GpuPlan:
         if self._lib.fabm_plan_set_virtual_shards(self._h, int(n_shards), ctypes_ref(st)) != nat.FABM_OK:
             _raise_status(st)
 
+    def emulate_shards(self, on: bool = True):
+        """Rank 0 of an attached plan: serve every shard from this one launch,
+        through the peers' IPC mappings (the sharded protocol across processes
+        where one GPU must host all ranks)."""
+        st = nat.Status()
+        if self._lib.fabm_plan_emulate_shards(self._h, int(bool(on)), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+
+    def shard_counters(self) -> tuple[int, int]:
+        """(src_done, bulk_tiles) of this plan's own control block."""
+        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        st = nat.Status()
+        if self._lib.fabm_plan_shard_counters(self._h, ctypes.byref(a), ctypes.byref(b), ctypes_ref(st)) != nat.FABM_OK:
+            _raise_status(st)
+        return int(a.value), int(b.value)
+
     def detach_shards(self):
         """Close the peer mappings and return to a single-GPU plan."""
         st = nat.Status()
