@@ -6,17 +6,19 @@
 // SM, 16 warps) integrates the whole sweep.  Work is cut into tickets taken
 // from one global counter, in ROUNDS J = 0 .. nb-1 (block J = steps
 // 128J .. 128J+127 of every trajectory):
-//   * PULL units (t, J, s), s < S_J = ceil(J / G): the bulk of block J's 128
-//     targets from source blocks [sG, min(sG+G, J)) -- Toeplitz chunks on the
+//   * PULL units (t, J, s), s < S_J: the bulk of block J's 128 targets from
+//     one segment of source blocks (pull_bounds: a body cut in pieces of G
+//     blocks, then a short tail ending at block J-1) -- Toeplitz chunks on the
 //     FP64 tensor cores (bulk_dmma.cuh) in ascending order -- into a partial
-//     slot part[t][s];
+//     slot part[t][J mod 2][s];
 //   * STEP units (t, J): the partials summed in slot order s = 0, 1, ..., then
 //     the 128 steps of the block: all 32 lanes run the sequential chain
 //     (serial.py:150-170) redundantly; lane l holds the sums of steps
 //     JB+4l..JB+4l+3 and pushes every new f_k into them (in-block window).
-// Within a round all pulls (s-major) precede all steps.  A pull waits for
-// step (t, J-1) (previous round: an earlier ticket, so its warp is running);
-// a step waits for its round's pulls (earlier tickets too): no deadlock.
+// Within a round all pulls (s-major) precede all steps.  A tail pull waits
+// for step (t, J-1), a body pull only for step (t, J-2) (earlier tickets, so
+// their warps are running); a step waits for its round's pulls (earlier
+// tickets too): no deadlock.
 // Splitting the pull over S_J warps keeps each trajectory's critical path
 // short (<= G chunks + 128 steps per round), so a few hundred trajectories
 // per GPU -- the 8-GPU share of the config 4 sweep -- still fill the machine.
@@ -51,24 +53,44 @@ struct BatchParams {
   int G;                    // pull segment length (source blocks)
   int S_max;                // pull segments of the largest round
   const long long* round_start;  // [nb + 1]: first ticket of round J
-  double* part;             // [T][S_max][B * 2 * DS]: partial bulk sums (DMMA lane-major layout)
-  int* pulls_done;          // [T]: completed pull units (cumulative over rounds)
+  const long long* pull_cum;     // [nb]: pull units of the rounds j <= J with j = J (mod 2)
+  double* part;             // [T][2][S_max][B * 2 * DS]: partial bulk sums by round parity (DMMA lane-major layout)
+  int* pulls_done;          // [T][2]: completed pull units by round parity (cumulative)
 };
 
-// pull units of round J: S_J = ceil(J / G), segment s = sources [sG, min(sG + G, J))
-__device__ __forceinline__ int pull_units(int J, int G) { return (J + G - 1) / G; }
-// pull units of rounds 0..J of one trajectory: sum_{j <= J} ceil(j / G)
-__device__ __forceinline__ long long pulls_through(int J, int G) {
-  const long long q = J / G, r = J % G;
-  return G * q * (q + 1) / 2 + (q + 1) * r;
+// Round J's pull segments: the BODY [0, J - tl) in pieces of G source blocks,
+// then the TAIL [J - tl, J), tl = min(J, kBatchTail).  Only the tail needs the
+// block the previous step unit has just finished; the body pulls of round J
+// run while the steps of round J-1 do (their slots are double-buffered by
+// round parity), so a trajectory's critical path per round is a tail of
+// <= kBatchTail chunks plus its 128 steps.  Bounds depend on J only.
+#ifndef FABM_BATCH_TAIL
+#define FABM_BATCH_TAIL 2
+#endif
+constexpr int kBatchTail = FABM_BATCH_TAIL;
+__host__ __device__ __forceinline__ int batch_tail(int J) { return J < kBatchTail ? J : kBatchTail; }
+__host__ __device__ __forceinline__ int pull_units(int J, int G) {
+  const int tl = batch_tail(J);
+  return (J - tl + G - 1) / G + (tl > 0 ? 1 : 0);
+}
+__host__ __device__ __forceinline__ void pull_bounds(int J, int s, int G, int& lo, int& hi) {
+  const int tl = batch_tail(J);
+  const int nbody = (J - tl + G - 1) / G;
+  if (s < nbody) {
+    lo = s * G;
+    hi = (s + 1) * G < J - tl ? (s + 1) * G : J - tl;
+  } else {
+    lo = J - tl;
+    hi = J;
+  }
 }
 
 template <int D>
-__device__ __forceinline__ double* part_slot(const BatchParams& P, int t, int s) {
-  return P.part + (static_cast<long long>(t) * P.S_max + s) * kB * 2 * Stride<D>::value;
+__device__ __forceinline__ double* part_slot(const BatchParams& P, int t, int parity, int s) {
+  return P.part + ((static_cast<long long>(t) * 2 + parity) * P.S_max + s) * kB * 2 * Stride<D>::value;
 }
 
-// pull unit: sources [sG, min(sG + G, J)) into the targets of block J
+// pull unit (t, J, s): sources [lo, hi) into the targets of block J
 template <int D>
 __device__ void batch_pull(const BatchParams& P, DmmaSmem<D>& A, int t, int J, int s, int lane) {
   constexpr int DS = Stride<D>::value;
@@ -77,9 +99,10 @@ __device__ void batch_pull(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
   const double* F = P.F + static_cast<long long>(t) * (P.nb + 1) * kB * DS;
   DmmaAcc<D> acc;
   dmma_zero<D>(acc);
-  const int i1 = min((s + 1) * P.G, J);
-  for (int I = s * P.G; I < i1; ++I) dmma_chunk<D, true>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
-  dmma_spill<D>(part_slot<D>(P, t, s), 0, lane, acc);
+  int lo, hi;
+  pull_bounds(J, s, P.G, lo, hi);
+  for (int I = lo; I < hi; ++I) dmma_chunk<D, true>(wb, wa, F, A, J * kB, I * kB, J * kB, lane, acc);
+  dmma_spill<D>(part_slot<D>(P, t, J & 1, s), 0, lane, acc);
 }
 
 // spin until *flag >= want (acquire); false on abort or watchdog expiry
@@ -131,11 +154,11 @@ __device__ bool batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
     DmmaAcc<D> acc;
     dmma_zero<D>(acc);
     const int np = pull_units(J, P.G);
-    if (!batch_wait(P, &P.pulls_done[t], pulls_through(J, P.G), lane)) return false;
-    if (np > 0) dmma_reload<D>(part_slot<D>(P, t, 0), 0, lane, acc);
+    if (!batch_wait(P, &P.pulls_done[2 * t + (J & 1)], __ldg(P.pull_cum + J), lane)) return false;
+    if (np > 0) dmma_reload<D>(part_slot<D>(P, t, J & 1, 0), 0, lane, acc);
     for (int sg = 1; sg < np; ++sg) {
       DmmaAcc<D> pa;
-      dmma_reload<D>(part_slot<D>(P, t, sg), 0, lane, pa);
+      dmma_reload<D>(part_slot<D>(P, t, J & 1, sg), 0, lane, pa);
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -313,17 +336,20 @@ __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
     const long long idx = static_cast<long long>(u) - __ldg(P.round_start + J);
     if (idx < static_cast<long long>(P.T) * SJ) {  // ---- pull unit (t, J, s)
       const int s = static_cast<int>(idx / P.T), t = static_cast<int>(idx % P.T);
-      if (!batch_wait(P, &P.next_block[t], J, lane)) return;
+      // its sources complete, and its parity's slots consumed by step (t, J-2)
+      int lo, hi;
+      pull_bounds(J, s, P.G, lo, hi);
+      if (!batch_wait(P, &P.next_block[t], hi > J - 1 ? hi : J - 1, lane)) return;
       if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) batch_pull<D>(P, A, t, J, s, lane);
       __threadfence();
       __syncwarp();
-      if (lane == 0) atomicAdd(&P.pulls_done[t], 1);
+      if (lane == 0) atomicAdd(&P.pulls_done[2 * t + (J & 1)], 1);
     } else {  // ---- step unit (t, J)
       const int t = static_cast<int>(idx - static_cast<long long>(P.T) * SJ);
       if (!batch_wait(P, &P.next_block[t], J, lane)) return;
       if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) {
         if (!batch_unit<SYS, D>(P, A, t, J, lane)) return;
-      } else if (!batch_wait(P, &P.pulls_done[t], pulls_through(J, P.G), lane)) {
+      } else if (!batch_wait(P, &P.pulls_done[2 * t + (J & 1)], __ldg(P.pull_cum + J), lane)) {
         return;  // a dead trajectory's pulls still finish before the slots are reused
       }
       __threadfence();

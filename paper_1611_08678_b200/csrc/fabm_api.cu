@@ -923,20 +923,26 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
     for (int c = 0; c < D; ++c) hy0[static_cast<size_t>(t) * kMaxDim + c] = problems[t].y0[c];
     for (int i = 0; i < kMaxParams; ++i) hprm[static_cast<size_t>(t) * kMaxParams + i] = problems[t].params[i];
   }
-  // pull segments: G source blocks per pull unit (batch.cuh); the ticket
-  // layout of round J is T * S_J pulls then T steps, S_J = ceil(J / G)
+  // pull segments: a body in pieces of G source blocks and a short tail
+  // (batch.cuh pull_bounds); the ticket layout of round J is T * S_J pulls
+  // then T steps
 #ifndef FABM_BATCH_G
 #define FABM_BATCH_G 32
 #endif
   constexpr int kPullG = FABM_BATCH_G;
-  const int S_max = std::max(1, (nb - 1 + kPullG - 1) / kPullG);
-  std::vector<long long> hround(nb + 1, 0);
-  for (int J = 0; J < nb; ++J) hround[J + 1] = hround[J] + static_cast<long long>(T) * ((J + kPullG - 1) / kPullG + 1);
+  int S_max = 1;
+  std::vector<long long> hround(nb + 1, 0), hcum(nb, 0);
+  for (int J = 0; J < nb; ++J) {
+    const int SJ = pull_units(J, kPullG);
+    S_max = std::max(S_max, SJ);
+    hround[J + 1] = hround[J] + static_cast<long long>(T) * (SJ + 1);
+    hcum[J] = (J >= 2 ? hcum[J - 2] : 0) + SJ;  // pulls of the rounds j <= J of J's parity
+  }
   StreamHolder stream_holder;
   CUDA_TRY(cudaStreamCreateWithFlags(&stream_holder.s, cudaStreamNonBlocking));
   cudaStream_t stream = stream_holder.s;
   retain_pool_memory(device);
-  DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl, dround, dpart, dpdone;
+  DevBuf dal, dg1, dg2, dha, dig, dy0, dprm, dW, dF, dY, dFc, dyl, dnext, dek, des, dtk, dctrl, dround, dcum, dpart, dpdone;
   const size_t szF = sizeof(double) * static_cast<size_t>(T) * (nb + 1) * kB * DS;
   const size_t szY = sizeof(double) * static_cast<size_t>(T) * (N + 1) * D;
   CUDA_TRY(dal.alloc(sizeof(double) * T, stream));
@@ -957,8 +963,9 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   CUDA_TRY(dtk.alloc(sizeof(unsigned long long), stream));
   CUDA_TRY(dctrl.alloc(sizeof(DevCtrl), stream));
   CUDA_TRY(dround.alloc(sizeof(long long) * (nb + 1), stream));
-  CUDA_TRY(dpart.alloc(sizeof(double) * static_cast<size_t>(T) * S_max * kB * 2 * DS, stream));
-  CUDA_TRY(dpdone.alloc(sizeof(int) * T, stream));
+  CUDA_TRY(dcum.alloc(sizeof(long long) * nb, stream));
+  CUDA_TRY(dpart.alloc(sizeof(double) * static_cast<size_t>(T) * 2 * S_max * kB * 2 * DS, stream));
+  CUDA_TRY(dpdone.alloc(sizeof(int) * 2 * T, stream));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -979,8 +986,9 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   cudaMemsetAsync(des.p, 0, sizeof(long long) * T, stream);
   cudaMemsetAsync(dtk.p, 0, sizeof(unsigned long long), stream);
   cudaMemsetAsync(dctrl.p, 0, sizeof(DevCtrl), stream);
-  cudaMemsetAsync(dpdone.p, 0, sizeof(int) * T, stream);
+  cudaMemsetAsync(dpdone.p, 0, sizeof(int) * 2 * T, stream);
   cudaMemcpyAsync(dround.p, hround.data(), sizeof(long long) * (nb + 1), cudaMemcpyHostToDevice, stream);
+  cudaMemcpyAsync(dcum.p, hcum.data(), sizeof(long long) * nb, cudaMemcpyHostToDevice, stream);
   {
     const long long total = static_cast<long long>(T) * WL;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 64));
@@ -1011,6 +1019,7 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   P.G = kPullG;
   P.S_max = S_max;
   P.round_start = dround.as<long long>();
+  P.pull_cum = dcum.as<long long>();
   P.part = dpart.as<double>();
   P.pulls_done = dpdone.as<int>();
   cudaEventRecord(e0, stream);
