@@ -155,6 +155,8 @@ __device__ bool batch_unit(const BatchParams& P, DmmaSmem<D>& A, int t, int J, i
     dmma_zero<D>(acc);
     const int np = pull_units(J, P.G);
     if (!batch_wait(P, &P.pulls_done[2 * t + (J & 1)], __ldg(P.pull_cum + J), lane)) return false;
+    // no pull of a later round of this parity can have counted yet (it waits for this step)
+    FABM_CHECK(P, lane != 0 || ld_relaxed_gpu(&P.pulls_done[2 * t + (J & 1)]) == __ldg(P.pull_cum + J));
     if (np > 0) dmma_reload<D>(part_slot<D>(P, t, J & 1, 0), 0, lane, acc);
     for (int sg = 1; sg < np; ++sg) {
       DmmaAcc<D> pa;
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) abm_batch_kernel(BatchParams P) {
       // its sources complete, and its parity's slots consumed by step (t, J-2)
       int lo, hi;
       pull_bounds(J, s, P.G, lo, hi);
+      FABM_CHECK(P, s < P.S_max && 0 <= lo && lo < hi && hi <= J && t < P.T);
       if (!batch_wait(P, &P.next_block[t], hi > J - 1 ? hi : J - 1, lane)) return;
       if (*((volatile int*)&P.err_kind[t]) == KIND_NONE) batch_pull<D>(P, A, t, J, s, lane);
       __threadfence();

@@ -77,7 +77,8 @@ struct DevCtrl {
   unsigned long long leader_throttle_ns;
   unsigned long long bulk_claims;  // units taken by a claimer (not their owner)
   unsigned long long prof[8];  // FABM_PROFILE builds: leader phase cycles
-  int pad2[14];
+  int check_line;          // FABM_CHECKED builds: source line of the first violated invariant
+  int pad2[13];
 };
 
 // One shard = the bulk agents of one GPU.  Every shard holds a full copy of
@@ -125,6 +126,9 @@ struct EngineParams {
   // slots, per-target counts of finished non-final units and of stage-2
   // arrivals, per-(class, column) claim cursors
   int k_max;               // highest segment class of this run
+  long long n_units;       // allocated unit slots / claim words (FABM_CHECKED bounds)
+  long long wlen;          // allocated weight entries
+  long long f_rows;        // allocated f history rows (per shard copy)
   int* claim;
   int* tdone;
   int* tstage;
@@ -154,6 +158,24 @@ __device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int
     for (int s = 0; s < P.n_shards; ++s) atomicExch_system(&P.shard[s].ctrl->abort, 1);
   }
 }
+
+// FABM_CHECKED builds (tools/checked_sweep.sh): bounds and protocol
+// invariants of the engine, the substitute for compute-sanitizer (closed on
+// this GPU pool).  A violation records its source line and aborts the run;
+// fabm_plan_run then reports it.  Compiled out otherwise.
+#ifdef FABM_CHECKED
+#define FABM_CHECK(P, cond)                                                      \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      atomicCAS(&(P).ctrl->check_line, 0, __LINE__);                            \
+      atomicExch(&(P).ctrl->abort, 1);                                           \
+    }                                                                            \
+  } while (0)
+#else
+#define FABM_CHECK(P, cond) \
+  do {                      \
+  } while (0)
+#endif
 
 // ======================================================================
 // STEPPER CTA
@@ -714,6 +736,7 @@ FABM_NI_OTHERS __device__ void stepper_writer(const EngineParams& P, StepperSmem
       return;
     }
     if (k <= kend) {
+      FABM_CHECK(P, k >= 0 && k <= N && k < P.f_rows);
       const int ri = static_cast<int>(k % kRing);
       double yf[2 * D];
       ld_pairs<D>(&S.ring[ri][0], yf);
@@ -971,7 +994,11 @@ __device__ __forceinline__ void publish_target(const EngineParams& P, int J, int
 // second arrival at stage 2 of target J's reduction?
 __device__ __forceinline__ bool stage2_second(const EngineParams& P, int J, int lane, bool sys) {
   int second = 0;
-  if (lane == 0) second = at_add(&P.tstage[J], 1, sys) == 1;
+  if (lane == 0) {
+    const int old = at_add(&P.tstage[J], 1, sys);
+    FABM_CHECK(P, old == 0 || old == 1);
+    second = old == 1;
+  }
   second = __shfl_sync(0xffffffffu, second, 0);
   if (second) fence_scope(sys);
   return second != 0;
@@ -991,6 +1018,13 @@ __device__ void unit_finish(const EngineParams& P, int J, int s, long long uid, 
   fence_scope(sys);
   __syncwarp();
   const long long base = unit_base(P, J);
+#ifdef FABM_CHECKED
+  // each unit finishes exactly once: its claim word turns negative here
+  if (lane == 0) {
+    const int w = ld_rlx(&P.claim[uid], sys);
+    FABM_CHECK(P, w > 0 && at_cas(&P.claim[uid], w, -w, sys) == w);
+  }
+#endif
   if (s == nseg - 1) {  // the final unit: P + p_final if the prefix is already there
     if (!stage2_second(P, J, lane, sys)) return;
     dmma_add_slot<D>(unit_slot<D>(P, base), lane, acc);  // p_final + P == P + p_final (IEEE add commutes)
@@ -998,7 +1032,11 @@ __device__ void unit_finish(const EngineParams& P, int J, int s, long long uid, 
     return;
   }
   int last = 0;
-  if (lane == 0) last = at_add(&P.tdone[J], 1, sys) == nseg - 2;
+  if (lane == 0) {
+    const int old = at_add(&P.tdone[J], 1, sys);
+    FABM_CHECK(P, old >= 0 && old <= nseg - 2);
+    last = old == nseg - 2;
+  }
   last = __shfl_sync(0xffffffffu, last, 0);
   if (!last) return;
   fence_scope(sys);
@@ -1205,6 +1243,12 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       }
     }
     const long long uid = unit_base(P, J) + s;
+    FABM_CHECK(P, J >= kL && J < nb && s >= 0 && s * (1 << seg_class(J - kL + 1)) <= nx && nx <= hi &&
+                      hi <= J - kL + 1 && uid >= 0 && uid < P.n_units);
+    FABM_CHECK(P, lane != 0 || ld_rlx(&P.claim[uid], sys) == agent + 1);  // only the unit's claimant computes it
+    // the chunk's weight window [128(J-nx)-127, 128(J-nx)+128] and f rows < 128(J-L+1) are allocated
+    FABM_CHECK(P, 128LL * (J - nx) - 127 >= 0 && 128LL * (J - nx) + 128 < P.wlen &&
+                      128LL * (J - kL + 1) <= P.f_rows);
     if (uid != cur_uid) {
       if (cur_uid >= 0) dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
       const int S = 1 << seg_class(J - kL + 1);

@@ -471,6 +471,9 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
     // the other GPUs of a sharded run)
     char* base0 = p->peer[0];
     P.k_max = p->k_max;
+    P.n_units = p->n_units;
+    P.wlen = p->wlen;
+    P.f_rows = static_cast<long long>(p->nb + 1) * kB;
     P.claim = reinterpret_cast<int*>(base0 + p->off_claim);
     P.tdone = reinterpret_cast<int*>(base0 + p->off_tdone);
     P.tstage = reinterpret_cast<int*>(base0 + p->off_tstage);
@@ -528,6 +531,10 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
         h.err_t = v.err_t;
       }
     }
+  }
+  if (h.check_line) {  // FABM_CHECKED build: an invariant failed (engine.cuh line)
+    set_status(status, FABM_ERR_CONFIG, "FABM_CHECKED: engine invariant violated at engine.cuh:%d", h.check_line);
+    return FABM_ERR_CONFIG;
   }
   if (h.err_code == ERR_OK && h.abort) {  // stopped by a peer shard (its watchdog or its error)
     h.err_code = ERR_TIMEOUT;
@@ -1044,6 +1051,10 @@ int fabm_solve_batch(const fabm_problem* problems, const fabm_grid* grids, int64
   DevCtrl hc{};
   cudaMemcpy(&hc, dctrl.p, sizeof(DevCtrl), cudaMemcpyDeviceToHost);
   cleanup();
+  if (hc.check_line) {
+    set_status(status, FABM_ERR_CONFIG, "FABM_CHECKED: batch invariant violated at batch.cuh:%d", hc.check_line);
+    return FABM_ERR_CONFIG;
+  }
   if (hc.err_code == ERR_TIMEOUT) {
     set_status(status, FABM_ERR_TIMEOUT, "batch watchdog expired");
     return FABM_ERR_TIMEOUT;
