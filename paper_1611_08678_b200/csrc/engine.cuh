@@ -1090,6 +1090,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
   const int n_targets = nb - kL;  // targets J = L .. nb-1
   if (n_targets <= 0) return;
   if (P.debug & 8) return;  // dev: no bulk agents (results invalid; the run reports FABM_ERR_CONFIG)
+  FABM_CHECK(P, !(P.debug & 16));  // dev: positive control of the FABM_CHECKED reporting path
   const bool sys = P.n_shards > 1;
   const int nA = P.n_agents;
   const int nown = owned_count(agent, nA, n_targets);

@@ -14,3 +14,15 @@ cd "$(dirname "$0")/.."
 FABM_LIBRARY=paper_1611_08678_b200/libfabm_checked.so FABM_RANDOM_CASES=${1:-200} \
   python -m pytest tests/test_gpu_random.py tests/test_gpu_headline_regime.py tests/test_gpu_sharded.py \
   tests/test_gpu_batch.py -q -x
+# positive control: a deliberately failed check must surface as an error
+FABM_LIBRARY=paper_1611_08678_b200/libfabm_checked.so FABM_DEBUG_MODE=16 python - <<'PY'
+import paper_1611_08678_b200 as fabm
+p = fabm.FractionalProblem(alpha=0.9, dim=3, rhs=fabm.rhs_lorenz(), y0=(1.0, 1.0, 1.0), t_end=2.0)
+try:
+    fabm.solve_gpu(p, p.grid(2000))
+except ValueError as exc:
+    assert "FABM_CHECKED" in str(exc), exc
+    print("positive control:", exc)
+else:
+    raise SystemExit("the checked build did not report the deliberate violation")
+PY
