@@ -933,9 +933,9 @@ __device__ __forceinline__ int seg_class(int n) {
 }
 __device__ __forceinline__ int class_lo(int k) { return k == 0 ? 1 : 1 << (k + 4); }  // n range [lo, hi)
 __device__ __forceinline__ int class_hi(int k) { return 1 << (k + 5); }
-__device__ __forceinline__ long long seg_prefix(long long m, int S) {  // sum_{n'=1..m} ceil(n'/S)
-  const long long q = m / S, r = m % S;
-  return static_cast<long long>(S) * q * (q + 1) / 2 + r * (q + 1);
+__device__ __forceinline__ long long seg_prefix(int m, int k) {  // sum_{n'=1..m} ceil(n'/2^k)
+  const long long q = m >> k, r = m & ((1 << k) - 1);
+  return ((q * (q + 1)) << k) / 2 + r * (q + 1);
 }
 // units of the classes below k: class 0 (n = 1..31, S = 1) has 496, class
 // j >= 1 (n = 16S..32S-1) has sum_{q=16..31} (qS + S - 1) = 392 S - 16
@@ -945,8 +945,8 @@ __host__ __device__ __forceinline__ long long class_base(int k) {
 // unit id of (J, 0): units of targets L .. J-1
 __device__ __forceinline__ long long unit_base(const EngineParams&, int J) {
   const int n = J - kL + 1;
-  const int k = seg_class(n), S = 1 << k;
-  return class_base(k) + seg_prefix(n - 1, S) - seg_prefix(class_lo(k) - 1, S);
+  const int k = seg_class(n);
+  return class_base(k) + seg_prefix(n - 1, k) - seg_prefix(class_lo(k) - 1, k);
 }
 
 __device__ __forceinline__ int owned_target(int agent, int i, int nA) { return kL + agent + i * nA; }
@@ -1061,6 +1061,9 @@ __device__ void unit_finish(const EngineParams& P, int J, int s, long long uid, 
 __device__ __forceinline__ int scan_claimable(const EngineParams& P, int M, int lane, bool sys, int& kc, int& kk,
                                               int& cc) {
   const int nend_all = P.nb - kL + 1;  // n < nend_all
+  // every target J <= M-1 is complete (the stepper passed it): a class whose
+  // last target is below M has nothing left to claim
+  while (kc <= P.k_max && class_hi(kc) + kL - 2 < M) ++kc;
   for (int k = kc; k <= P.k_max; ++k) {
     const int S = 1 << k;
     const int nend = min(class_hi(k), nend_all);
@@ -1138,10 +1141,10 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       bool pend = false, elig = false;
       if (i < nown) {
         const int J = owned_target(agent, i, nA);
-        const int n = J - kL + 1;
-        const int S = 1 << seg_class(n);
+        const int n = owned_target(agent, i, nA) - kL + 1;
+        const int k = seg_class(n);
         const int nx = A.own_next[i] >> 1;
-        const int uhi = min((nx / S + 1) * S, n);
+        const int uhi = min(((nx >> k) + 1) << k, n);
         const int avail = min(uhi, M) - nx;
         pend = avail > 0;
         elig = pend && (avail >= kOwnBatch || uhi <= M || J - M <= kUrgent);
@@ -1187,7 +1190,6 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       }
       continue;
     }
-    last_progress = global_ns();
     int J, s, nx, hi, lim;
     if (take_dyn) {
       if (dJ < 0) {
@@ -1227,11 +1229,11 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     } else {
       J = owned_target(agent, best, nA);
       const int n = J - kL + 1;
-      const int S = 1 << seg_class(n);
+      const int k = seg_class(n);
       const int v = A.own_next[best];
       nx = v >> 1;
-      s = nx / S;
-      hi = min((s + 1) * S, n);
+      s = nx >> k;
+      hi = min((s + 1) << k, n);
       lim = min(hi, M);
       if (!(v & 1)) {  // first touch of this unit: claim it (a claimer may hold it)
         int ok = 0;
@@ -1252,8 +1254,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
                       128LL * (J - kL + 1) <= P.f_rows);
     if (uid != cur_uid) {
       if (cur_uid >= 0) dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
-      const int S = 1 << seg_class(J - kL + 1);
-      if (nx > s * S) {
+      if (nx > (s << seg_class(J - kL + 1))) {
         __syncwarp();
         dmma_reload_slot<D>(unit_slot<D>(P, uid), lane, acc);
       } else {
