@@ -79,6 +79,7 @@ struct DevCtrl {
   unsigned long long prof[8];  // FABM_PROFILE builds: leader phase cycles
   int check_line;          // FABM_CHECKED builds: source line of the first violated invariant
   int pad2[13];
+  unsigned long long prof2[8];  // FABM_PROFILE builds: agent event counts / cycles (tools/prof_bulk.py)
 };
 
 // One shard = the bulk agents of one GPU.  Every shard holds a full copy of
@@ -1112,9 +1113,12 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
 
 #ifdef FABM_PROFILE
   long long c_tile = 0, c_idle = 0, c_sw = 0, c_t = clock64();
+  unsigned long long n_sel = 0, n_scan = 0, n_spill = 0, n_reload = 0, n_fin = 0, c_fin = 0, c_scan = 0, n_idle = 0;
 #define APROF(var) { const long long _t = clock64(); var += _t - c_t; c_t = _t; }
+#define ACOUNT(var) ++var;
 #else
 #define APROF(var)
+#define ACOUNT(var)
 #endif
   while (true) {
     int M = 0, ab = 0;
@@ -1166,11 +1170,19 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     } else if (Jo > dyn_lb || (M >> kc) != (lb_M >> kc) || lb_M < 0) {
       // a column of a class >= kc completes only when M crosses a multiple
       // of its segment length 2^k, k >= kc
+#ifdef FABM_PROFILE
+      const long long t_sc = clock64();
+#endif
       Jd = scan_claimable(P, M, lane, sys, kc, kd, cd);
+#ifdef FABM_PROFILE
+      c_scan += clock64() - t_sc;
+      ++n_scan;
+#endif
       dyn_lb = Jd;
       lb_M = M;
     }
     const bool take_dyn = Jd < Jo;
+    ACOUNT(n_sel)
     if (!take_dyn && best < 0) best = any;  // nothing eligible or claimable: a lone pending chunk
     if (!take_dyn && best < 0) {
       // nothing to do: finished, or wait for the next source block
@@ -1182,6 +1194,7 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       }
       if (fin) break;
       __nanosleep(256);
+      ACOUNT(n_idle)
       if ((++idle_polls & 63) == 0) lb_M = -1;  // re-scan now and then (exit detection)
       APROF(c_idle)
       if (global_ns() - last_progress > P.timeout_ns) {
@@ -1253,10 +1266,14 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     FABM_CHECK(P, 128LL * (J - nx) - 127 >= 0 && 128LL * (J - nx) + 128 < P.wlen &&
                       128LL * (J - kL + 1) <= P.f_rows);
     if (uid != cur_uid) {
-      if (cur_uid >= 0) dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
+      if (cur_uid >= 0) {
+        dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
+        ACOUNT(n_spill)
+      }
       if (nx > (s << seg_class(J - kL + 1))) {
         __syncwarp();
         dmma_reload_slot<D>(unit_slot<D>(P, uid), lane, acc);
+        ACOUNT(n_reload)
       } else {
         dmma_zero<D>(acc);
       }
@@ -1285,7 +1302,14 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     }
     __syncwarp();
     if (nx == hi) {
+#ifdef FABM_PROFILE
+      const long long t_f = clock64();
+#endif
       unit_finish<D>(P, J, s, uid, lane, acc, sys);
+#ifdef FABM_PROFILE
+      c_fin += clock64() - t_f;
+      ++n_fin;
+#endif
       cur_uid = -1;
       if (take_dyn) dJ = -1;
     }
@@ -1299,6 +1323,8 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[4]), (unsigned long long)c_tile);
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[5]), (unsigned long long)c_idle);
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[6]), (unsigned long long)c_sw);
+    const unsigned long long ev[8] = {n_sel, n_scan, n_spill, n_reload, n_fin, c_fin, c_scan, n_idle};
+    for (int q = 0; q < 8; ++q) atomicAdd(&P.ctrl->prof2[q], ev[q]);
   }
 #endif
 }

@@ -172,9 +172,12 @@ long long host_unit_base(int J) {
 
 }  // namespace
 
-static unsigned long long g_last_prof[8];
+static unsigned long long g_last_prof[16];
 extern "C" void fabm_debug_prof(unsigned long long* out) {
   for (int i = 0; i < 8; ++i) out[i] = g_last_prof[i];
+}
+extern "C" void fabm_debug_prof2(unsigned long long* out) {
+  for (int i = 0; i < 8; ++i) out[i] = g_last_prof[8 + i];
 }
 #ifdef FABM_PROFILE
 static unsigned long long* g_trace = nullptr;
@@ -549,6 +552,7 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
   p->stats.leader_wait_ns = static_cast<int64_t>(h.leader_wait_ns);
   p->stats.leader_throttle_ns = static_cast<int64_t>(h.leader_throttle_ns);
   for (int i = 0; i < 8; ++i) g_last_prof[i] = h.prof[i];
+  for (int i = 0; i < 8; ++i) g_last_prof[8 + i] = h.prof2[i];
   if (h.err_code != ERR_OK) {
     if (status) {
       status->code = h.err_code == ERR_TIMEOUT ? FABM_ERR_TIMEOUT : FABM_ERR_NONFINITE;

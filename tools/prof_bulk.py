@@ -15,4 +15,12 @@ for N in [int(x) for x in (sys.argv[1:] or ["300000", "1000000"])]:
     cyc = ms * 1e-3 * 1.965e9
     print(f"N={N} kernel={ms:.1f}ms steps/s={N/(ms*1e-3):.3e} wait={st['leader_wait_ns']/1e6:.1f}ms "
           f"agents={agents} tile={buf[4]/agents/cyc:.3f} idle={buf[5]/agents/cyc:.3f} switch={buf[6]/agents/cyc:.3f} (fractions of kernel time per agent)", flush=True)
+    if hasattr(lib, "fabm_debug_prof2"):
+        b2 = (ctypes.c_ulonglong * 8)()
+        lib.fabm_debug_prof2(b2)
+        n_sel, n_scan, n_spill, n_reload, n_fin, c_fin, c_scan, n_idle = list(b2)
+        print(f"   per agent: selections {n_sel/agents:.0f}, cursor scans {n_scan/agents:.0f} ({c_scan/agents/cyc:.3f} of "
+              f"kernel time), spills {n_spill/agents:.0f}, reloads {n_reload/agents:.0f}, units finished "
+              f"{n_fin/agents:.0f} ({c_fin/agents/cyc:.3f} of kernel time), idle polls {n_idle/agents:.0f}; "
+              f"tiles {st['bulk_tiles']/agents:.0f}, claims {st['bulk_claims']}", flush=True)
     plan.close()
