@@ -287,6 +287,45 @@ struct LeaderState {
 // near sums of step m1 (owner lane -> all lanes via smem) and its far handoff.
 // ROT: a chunk rotation is possible at this step (the fast block path knows
 // statically where the 32-step chunk boundaries can fall).
+#ifndef FABM_FAR_AT_ROT
+#define FABM_FAR_AT_ROT 1
+#endif
+// FABM_FAR_AT_ROT: the far handoffs of a whole 32-step chunk are folded into
+// the lanes' near sums once, when the chunk becomes current (lane l: step
+// c0 + l), instead of one handoff read and 2d adds per step on the chain.
+// The helpers hand a chunk off ~30 steps before it starts, so this waits
+// only when the bulk of the chunk's block is late.  false on abort/timeout.
+template <int D>
+__device__ __forceinline__ bool leader_absorb_far(const EngineParams& P, StepperSmem& S, LeaderState<D>& st, int c0,
+                                               int lane, unsigned long long& waited) {
+  const int m = c0 + lane;
+  const bool live = m < static_cast<int>(P.N);  // the helpers hand off steps m < N
+  const int slot = m & (kHR - 1);
+  if (!__all_sync(0xffffffffu, !live || ld_volatile_smem(&S.hflag[slot]) == m)) {
+    const unsigned long long w0 = global_ns();
+    unsigned spins = 0;
+    while (!__all_sync(0xffffffffu, !live || ld_volatile_smem(&S.hflag[slot]) == m)) {
+      if (((++spins) & 1023u) == 0) {
+        if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
+        if (global_ns() - w0 > P.timeout_ns) {
+          if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, c0, 0.0);
+          st_volatile_smem(&S.abort, 1);
+          return false;
+        }
+      }
+    }
+    waited += global_ns() - w0;
+  }
+  __threadfence_block();  // acquire: the helpers release hflag after writing hbuf
+  if (live) {
+    double fr[2 * D];
+    ld_pairs<D>(&S.hbuf[slot][0], fr);
+#pragma unroll
+    for (int c = 0; c < 2 * D; ++c) st.accA[c] = st.accA[c] + fr[c];
+  }
+  return true;
+}
+
 template <int D, bool ROT>
 __device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st, int m1, int lane, double* nr,
                                              double* fr, bool acquire_flag) {
@@ -302,7 +341,7 @@ __device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st,
   const int slot = m1 & (kHR - 1);
   const int fl = acquire_flag ? ld_acquire_cta_smem(&S.hflag[slot]) : m1;
   ld_pairs<D>(xb, nr);
-  ld_pairs<D>(&S.hbuf[slot][0], fr);
+  if (!FABM_FAR_AT_ROT) ld_pairs<D>(&S.hbuf[slot][0], fr);
   return fl;
 }
 
@@ -346,7 +385,18 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
                                             unsigned long long& waited) {
   const int m1 = n + 1;
   double nr[2 * D], fr[2 * D];
+#if FABM_FAR_AT_ROT
+  if (ROT && (m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation, far parts folded in
+#pragma unroll
+    for (int c = 0; c < 2 * D; ++c) { st.accA[c] = st.accB[c]; st.accB[c] = 0.0; }
+    st.cA += 1;
+    if (!leader_absorb_far<D>(P, S, st, m1, lane, waited)) return false;
+  }
+  leader_gather<D, false>(S, st, m1, lane, nr, fr, false);
+  const int fl = m1;
+#else
   const int fl = leader_gather<D, ROT>(S, st, m1, lane, nr, fr, !FAST);
+#endif
   const PushW pw = leader_push_weights<false>(S, st.cA, m1, lane);
   const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
   const double ha = P.ha;
@@ -374,6 +424,15 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   for (int c = 0; c < D; ++c) st.fc[c] = v[D + c];
   // non-finite rhs outputs are detected by the writer warp on the published
   // rows (fP and f of every step), off the chain's SMSP
+#if FABM_FAR_AT_ROT
+  (void)fl;
+  // pre-sums of step n+1: the owner's near sum, far part included at rotation
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    st.preP[c] = nr[c];
+    st.preC[c] = nr[D + c];
+  }
+#else
   // slow path: the far handoff of step n+1 was not ready when read
   if (!FAST && m1 < P.N && fl != m1) {
     if (!leader_wait_handoff(P, S, m1, waited)) return false;
@@ -386,6 +445,7 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
     st.preP[c] = nr[c] + fr[c];
     st.preC[c] = nr[D + c] + fr[D + c];
   }
+#endif
   return true;
 }
 
@@ -460,6 +520,18 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
 
   // step 0: its pre-sums are the far handoff alone (c_0 f_0); then f_0 enters
   // the near sums of steps 1..63
+#if FABM_FAR_AT_ROT
+  if (!leader_absorb_far<D>(P, S, st, 0, lane, waited)) return;  // chunk 0: the first-node terms c_m f_0
+  {
+    double nr[2 * D], fr[2 * D];
+    leader_gather<D, false>(S, st, 0, lane, nr, fr, false);
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      st.preP[c] = nr[c];
+      st.preC[c] = nr[D + c];
+    }
+  }
+#else
   if (!leader_wait_handoff(P, S, 0, waited)) return;
   {
     double nr[2 * D], fr[2 * D];
@@ -470,6 +542,7 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
       st.preC[c] = nr[D + c] + fr[D + c];
     }
   }
+#endif
   leader_push<D>(st, leader_push_weights<true>(S, st.cA, 0, lane), f0);
 #pragma unroll
   for (int c = 0; c < D; ++c) st.fc[c] = f0[c];
@@ -486,7 +559,7 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
     if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
   if (!leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   while (n + 8 <= N32) {
-    if (solo || leader_block_ready(S, n)) {
+    if (FABM_FAR_AT_ROT || solo || leader_block_ready(S, n)) {
       ++fast_blocks;
       // n % 8 == 0: a 32-step chunk boundary (m1 % 32 == 0) can only be the
       // last step, whose gather (step n+8) is checked on its own
@@ -928,6 +1001,10 @@ constexpr int kDynBurst = FABM_DYN_BURST;  // chunks of a claimed unit between s
 #endif
 constexpr int kOwnBatch = FABM_OWN_BATCH;  // frontier chunks taken together (unless urgent)
 constexpr int kUrgent = FABM_URGENT;       // blocks before a target's deadline that make any chunk urgent
+#ifndef FABM_STICKY_OWN
+#define FABM_STICKY_OWN 0
+#endif
+constexpr bool kStickyOwn = FABM_STICKY_OWN;
 __device__ __forceinline__ int seg_class(int n) {
   const int k = 31 - __clz(n) - 4;
   return k > 0 ? k : 0;
@@ -1291,7 +1368,10 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       ++nx;
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
-      if (M2 != M && (!take_dyn || j_soon - M2 <= kUrgent)) break;  // a newer source block: re-run the selection
+      // a newer source block: re-run the selection (owned units at once --
+      // EDF may switch to an earlier target -- unless FABM_STICKY_OWN;
+      // claimed units only when an owned target nears its deadline)
+      if (M2 != M && ((!take_dyn && !kStickyOwn) || j_soon - M2 <= kUrgent)) break;
     }
     APROF(c_tile)
     __syncwarp();
