@@ -152,12 +152,18 @@ __device__ __forceinline__ void ctrl_abort(DevCtrl* ctrl, int code, int kind, lo
   __threadfence();
   atomicExch(&ctrl->abort, 1);
 }
-__device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int kind, long long step, double t) {
-  ctrl_abort(P.ctrl, code, kind, step, t);
-  if (P.n_shards > 1) {  // stop every shard (peer control blocks)
+// cold path, out of line (keeps the stepper's hot loops small in the
+// instruction cache; plain pointers, so P stays in the parameter space)
+__device__ __noinline__ void raise_abort_cold(DevCtrl* ctrl, const ShardView* shard, int n_shards, int code, int kind,
+                                              long long step, double t) {
+  ctrl_abort(ctrl, code, kind, step, t);
+  if (n_shards > 1) {  // stop every shard (peer control blocks)
     __threadfence_system();
-    for (int s = 0; s < P.n_shards; ++s) atomicExch_system(&P.shard[s].ctrl->abort, 1);
+    for (int s = 0; s < n_shards; ++s) atomicExch_system(&shard[s].ctrl->abort, 1);
   }
+}
+__device__ __forceinline__ void raise_abort(const EngineParams& P, int code, int kind, long long step, double t) {
+  raise_abort_cold(P.ctrl, P.shard, P.n_shards, code, kind, step, t);
 }
 
 // FABM_CHECKED builds (tools/checked_sweep.sh): bounds and protocol
