@@ -25,18 +25,6 @@
 #pragma once
 #include "device_common.cuh"
 
-// code-generation boundaries between the warp roles (register allocation
-// of one role must not depend on another's code)
-#ifndef FABM_NI_LEADER
-#define FABM_NI_LEADER
-#endif
-#ifndef FABM_NI_AGENT
-#define FABM_NI_AGENT
-#endif
-#ifndef FABM_NI_OTHERS
-#define FABM_NI_OTHERS
-#endif
-
 namespace fabm {
 
 // ------------------------------------------------------------ geometry
@@ -226,25 +214,6 @@ __device__ __forceinline__ int slowest_consumer(StepperSmem& S) {
   return lo;
 }
 
-// spin until the helpers handed off the far part of step m; false on abort/timeout
-__device__ __noinline__ bool leader_wait_handoff(const EngineParams& P, StepperSmem& S, long long m,
-                                                 unsigned long long& waited) {
-  const int slot = static_cast<int>(m % kHR);
-  const unsigned long long w0 = global_ns();
-  unsigned spins = 0;
-  while (ld_acquire_cta_smem(&S.hflag[slot]) != static_cast<int>(m)) {
-    if (((++spins) & 1023u) == 0) {
-      if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
-      if (global_ns() - w0 > P.timeout_ns) {
-        if ((threadIdx.x & 31) == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, m, 0.0);
-        st_volatile_smem(&S.abort, 1);
-        return false;
-      }
-    }
-  }
-  waited += global_ns() - w0;
-  return true;
-}
 
 // 2d doubles as d 16-byte vectors (2d is even for every d)
 template <int D>
@@ -293,10 +262,7 @@ struct LeaderState {
 // near sums of step m1 (owner lane -> all lanes via smem) and its far handoff.
 // ROT: a chunk rotation is possible at this step (the fast block path knows
 // statically where the 32-step chunk boundaries can fall).
-#ifndef FABM_FAR_AT_ROT
-#define FABM_FAR_AT_ROT 1
-#endif
-// FABM_FAR_AT_ROT: the far handoffs of a whole 32-step chunk are folded into
+// The far handoffs of a whole 32-step chunk are folded into
 // the lanes' near sums once, when the chunk becomes current (lane l: step
 // c0 + l), instead of one handoff read and 2d adds per step on the chain.
 // The helpers hand a chunk off ~30 steps before it starts, so this waits
@@ -332,23 +298,16 @@ __device__ __forceinline__ bool leader_absorb_far(const EngineParams& P, Stepper
   return true;
 }
 
-template <int D, bool ROT>
-__device__ __forceinline__ int leader_gather(StepperSmem& S, LeaderState<D>& st, int m1, int lane, double* nr,
-                                             double* fr, bool acquire_flag) {
-  if (ROT && (m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation A <- B, B <- 0
-#pragma unroll
-    for (int c = 0; c < 2 * D; ++c) { st.accA[c] = st.accB[c]; st.accB[c] = 0.0; }
-    st.cA += 1;
-  }
+// the pre-sums of step m1 (near + far): the owner lane's sums, to all lanes
+// through shared memory
+template <int D>
+__device__ __forceinline__ void leader_gather(StepperSmem& S, const LeaderState<D>& st, int m1, int lane,
+                                              double* nr) {
   const int owner = m1 & (kChunk - 1);
   double* xb = &S.xfer[m1 & 1][0];
   if (lane == owner) st_pairs<D>(xb, st.accA);
   __syncwarp();
-  const int slot = m1 & (kHR - 1);
-  const int fl = acquire_flag ? ld_acquire_cta_smem(&S.hflag[slot]) : m1;
   ld_pairs<D>(xb, nr);
-  if (!FABM_FAR_AT_ROT) ld_pairs<D>(&S.hbuf[slot][0], fr);
-  return fl;
 }
 
 // push f_k (k = m1, just computed) into the near sums of A and B; the padded
@@ -382,27 +341,21 @@ __device__ __forceinline__ void leader_push(LeaderState<D>& st, const PushW& w, 
 // the issue order the in-order warp needs: everything that does not depend on
 // this step's f (the gather of step n+1, its pre-sums, the push weights) is
 // issued before the chain so it completes under the chain's FP64 latencies.
-//   FAST: the caller verified every far handoff of the enclosing 8-step
-//         block (leader_block_ready) -- no per-step flag test or slow path;
-//   ROT:  a chunk rotation can happen at this step.
-template <int SYS, int D, bool FAST, bool ROT>
+//   ROT: a chunk rotation can happen at this step (the 8-step blocks know
+//        statically where the 32-step chunk boundaries can fall).
+template <int SYS, int D, bool ROT>
 __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, LeaderState<D>& st,
                                             double b0, double a0e, int n, int lane, uint32_t bars_u32,
                                             unsigned long long& waited) {
   const int m1 = n + 1;
-  double nr[2 * D], fr[2 * D];
-#if FABM_FAR_AT_ROT
   if (ROT && (m1 & (kChunk - 1)) == 0 && m1 > 0) {  // warp-uniform: chunk rotation, far parts folded in
 #pragma unroll
     for (int c = 0; c < 2 * D; ++c) { st.accA[c] = st.accB[c]; st.accB[c] = 0.0; }
     st.cA += 1;
     if (!leader_absorb_far<D>(P, S, st, m1, lane, waited)) return false;
   }
-  leader_gather<D, false>(S, st, m1, lane, nr, fr, false);
-  const int fl = m1;
-#else
-  const int fl = leader_gather<D, ROT>(S, st, m1, lane, nr, fr, !FAST);
-#endif
+  double nr[2 * D];
+  leader_gather<D>(S, st, m1, lane, nr);
   const PushW pw = leader_push_weights<false>(S, st.cA, m1, lane);
   const double t1 = static_cast<double>(m1) * P.h;  // (n + 1) * h, serial.py:151
   const double ha = P.ha;
@@ -430,46 +383,16 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
   for (int c = 0; c < D; ++c) st.fc[c] = v[D + c];
   // non-finite rhs outputs are detected by the writer warp on the published
   // rows (fP and f of every step), off the chain's SMSP
-#if FABM_FAR_AT_ROT
-  (void)fl;
-  // pre-sums of step n+1: the owner's near sum, far part included at rotation
+  // pre-sums of step n+1: the owner's near sum (far part included at the
+  // rotation), read now so the shared-memory loads complete under the chain
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     st.preP[c] = nr[c];
     st.preC[c] = nr[D + c];
   }
-#else
-  // slow path: the far handoff of step n+1 was not ready when read
-  if (!FAST && m1 < P.N && fl != m1) {
-    if (!leader_wait_handoff(P, S, m1, waited)) return false;
-    ld_pairs<D>(&S.hbuf[m1 & (kHR - 1)][0], fr);
-  }
-  // pre-sums of step n+1 = near + far, consumed after this step's chain so
-  // the shared-memory loads of the gather complete under it
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    st.preP[c] = nr[c] + fr[c];
-    st.preC[c] = nr[D + c] + fr[D + c];
-  }
-#endif
   return true;
 }
 
-// far handoffs of steps n+1 .. n+7 present?  (n % 8 == 0, n + 8 <= N: all
-// those steps are < N and lie in the 32-step chunk of n+1, whose handoff
-// happened ~25 steps ago.)  Plain loads issue in parallel; the fence then
-// orders the block's hbuf reads after them (fence-based acquire).
-__device__ __forceinline__ bool leader_block_ready(StepperSmem& S, int n) {
-  bool ok = true;
-#pragma unroll
-  for (int u = 1; u <= 7; ++u) {
-    const int m = n + u;
-    ok &= ld_volatile_smem(&S.hflag[m & (kHR - 1)]) == m;
-  }
-  ok = __all_sync(0xffffffffu, ok);
-  __threadfence_block();
-  return ok;
-}
 
 template <int D>
 __device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
@@ -499,7 +422,7 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
 }
 
 template <int SYS, int D>
-FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) {
+__device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) {
   const long long N = P.N;
   LeaderState<D> st;
   double f0[D];
@@ -526,29 +449,16 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
 
   // step 0: its pre-sums are the far handoff alone (c_0 f_0); then f_0 enters
   // the near sums of steps 1..63
-#if FABM_FAR_AT_ROT
   if (!leader_absorb_far<D>(P, S, st, 0, lane, waited)) return;  // chunk 0: the first-node terms c_m f_0
   {
-    double nr[2 * D], fr[2 * D];
-    leader_gather<D, false>(S, st, 0, lane, nr, fr, false);
+    double nr[2 * D];
+    leader_gather<D>(S, st, 0, lane, nr);
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       st.preP[c] = nr[c];
       st.preC[c] = nr[D + c];
     }
   }
-#else
-  if (!leader_wait_handoff(P, S, 0, waited)) return;
-  {
-    double nr[2 * D], fr[2 * D];
-    leader_gather<D, true>(S, st, 0, lane, nr, fr, true);
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      st.preP[c] = nr[c] + fr[c];
-      st.preC[c] = nr[D + c] + fr[D + c];
-    }
-  }
-#endif
   leader_push<D>(st, leader_push_weights<true>(S, st.cA, 0, lane), f0);
 #pragma unroll
   for (int c = 0; c < D; ++c) st.fc[c] = f0[c];
@@ -560,28 +470,22 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
   unsigned long long fast_blocks = 0, lag_sum = 0;
   int n = 0;
   // step 0 has no corrector interior (a0 term excluded); blocks start at 8
-  if (!leader_step<SYS, D, false, true>(P, S, st, b0, 0.0, 0, lane, bars_u32, waited)) return;
+  if (!leader_step<SYS, D, true>(P, S, st, b0, 0.0, 0, lane, bars_u32, waited)) return;
   for (n = 1; n < 8 && n < N32; ++n)
-    if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
   if (!leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   while (n + 8 <= N32) {
-    if (FABM_FAR_AT_ROT || solo || leader_block_ready(S, n)) {
-      ++fast_blocks;
-      // n % 8 == 0: a 32-step chunk boundary (m1 % 32 == 0) can only be the
-      // last step, whose gather (step n+8) is checked on its own
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 0, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 1, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 2, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 3, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 4, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 5, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, true, false>(P, S, st, b0, a0, n + 6, lane, bars_u32, waited)) return;
-      if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n + 7, lane, bars_u32, waited)) return;
-    } else {
-#pragma unroll 1
-      for (int u = 0; u < 8; ++u)
-        if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n + u, lane, bars_u32, waited)) return;
-    }
+    ++fast_blocks;
+    // n % 8 == 0: a 32-step chunk boundary (m1 % 32 == 0) can only be the
+    // last step of the block
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 0, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 1, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 2, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 3, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 4, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 5, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, false>(P, S, st, b0, a0, n + 6, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, true>(P, S, st, b0, a0, n + 7, lane, bars_u32, waited)) return;
     n += 8;
     // back-pressure / abort check every 16 steps (its 9 shared-memory loads
     // stall the in-order issue); the lag bound leaves room for 16 more steps
@@ -589,7 +493,7 @@ FABM_NI_LEADER __device__ void stepper_leader(const EngineParams& P, StepperSmem
   }
 #pragma unroll 1
   for (; n < N32; ++n)
-    if (!leader_step<SYS, D, false, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
+    if (!leader_step<SYS, D, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
   if (!solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   if (lane == 0) {
     P.ctrl->prof[0] = static_cast<unsigned long long>(clock64() - c_loop);
@@ -686,7 +590,7 @@ __device__ __forceinline__ void helper_batch(const StepperSmem& S, int k0, int k
 }
 
 template <int D>
-FABM_NI_OTHERS __device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, int hwarp) {
+__device__ void stepper_helper(const EngineParams& P, StepperSmem& S, int hid, int hwarp) {
   constexpr int NS = kSlotsPerThread;
   const int N = static_cast<int>(P.N);
   const int lane = threadIdx.x & 31;
@@ -773,7 +677,7 @@ FABM_NI_OTHERS __device__ void stepper_helper(const EngineParams& P, StepperSmem
 // of 32 steps; after the last row of a source block it raises io_block (CTA
 // scope, release).  It never touches slow global state, so it keeps pace.
 template <int D>
-FABM_NI_OTHERS __device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) {
+__device__ void stepper_writer(const EngineParams& P, StepperSmem& S, int lane) {
   constexpr int DS = Stride<D>::value;
   const long long N = P.N;
   long long k0 = 0;
@@ -852,7 +756,7 @@ FABM_NI_OTHERS __device__ void stepper_writer(const EngineParams& P, StepperSmem
 // from HBM into shared memory for the helpers.  All slow global round trips
 // of the stepper CTA live here, off the writer's and the leader's paths.
 template <int D>
-FABM_NI_OTHERS __device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lane) {
+__device__ void stepper_publisher(const EngineParams& P, StepperSmem& S, int lane) {
   constexpr int DS = Stride<D>::value;
   const int nb = P.nb;
   const int last_block = static_cast<int>(P.N / kB);  // complete source blocks at the end
@@ -995,22 +899,8 @@ namespace fabm {
 // p_{n-2} (usually long before the deadline), and whichever of {prefix,
 // final unit} arrives second adds the final unit's partial.
 constexpr int kMaxClasses = 32;
-#ifndef FABM_DYN_BURST
-#define FABM_DYN_BURST 4
-#endif
-constexpr int kDynBurst = FABM_DYN_BURST;  // chunks of a claimed unit between selections
-#ifndef FABM_OWN_BATCH
-#define FABM_OWN_BATCH 1
-#endif
-#ifndef FABM_URGENT
-#define FABM_URGENT 16
-#endif
-constexpr int kOwnBatch = FABM_OWN_BATCH;  // frontier chunks taken together (unless urgent)
-constexpr int kUrgent = FABM_URGENT;       // blocks before a target's deadline that make any chunk urgent
-#ifndef FABM_STICKY_OWN
-#define FABM_STICKY_OWN 0
-#endif
-constexpr bool kStickyOwn = FABM_STICKY_OWN;
+constexpr int kDynBurst = 4;  // chunks of a claimed unit between selections (8: 200 vs 182 ms at N=1e6)
+constexpr int kUrgent = 16;  // blocks before an owned target's deadline that end a claimed-unit burst
 __device__ __forceinline__ int seg_class(int n) {
   const int k = 31 - __clz(n) - 4;
   return k > 0 ? k : 0;
@@ -1172,7 +1062,7 @@ __device__ __forceinline__ int scan_claimable(const EngineParams& P, int M, int 
 }
 
 template <int D>
-FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
+__device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int lane, const ShardView& sv) {
   const int nb = P.nb;
   const int n_targets = nb - kL;  // targets J = L .. nb-1
   if (n_targets <= 0) return;
@@ -1217,34 +1107,24 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       last_progress = global_ns();
     }
     __syncwarp();
-    // earliest owned target with published chunks in its current unit.
-    // ELIGIBLE: a batch of >= kOwnBatch chunks, the rest of its unit, or a
-    // deadline within kUrgent blocks -- single frontier chunks of distant
-    // targets wait and are taken in batches (fewer spill/reload switches);
-    // PENDING (any published chunk) is the fallback before idling
-    int best = -1, any = -1;
+    // earliest owned target with a published chunk in its current unit
+    int best = -1;
     for (int b0 = 0; b0 < nown; b0 += 32) {
       const int i = b0 + lane;
-      bool pend = false, elig = false;
+      bool pend = false;
       if (i < nown) {
-        const int J = owned_target(agent, i, nA);
         const int n = owned_target(agent, i, nA) - kL + 1;
         const int k = seg_class(n);
         const int nx = A.own_next[i] >> 1;
         const int uhi = min(((nx >> k) + 1) << k, n);
-        const int avail = min(uhi, M) - nx;
-        pend = avail > 0;
-        elig = pend && (avail >= kOwnBatch || uhi <= M || J - M <= kUrgent);
+        pend = nx < min(uhi, M);
       }
-      const unsigned balp = __ballot_sync(0xffffffffu, pend);
-      const unsigned bale = __ballot_sync(0xffffffffu, elig);
-      if (any < 0 && balp) any = b0 + __ffs(balp) - 1;
-      if (bale) { best = b0 + __ffs(bale) - 1; break; }
+      const unsigned bal = __ballot_sync(0xffffffffu, pend);
+      if (bal) { best = b0 + __ffs(bal) - 1; break; }
     }
     const int Jo = best >= 0 ? owned_target(agent, best, nA) : 0x7fffffff;
-    // nearest deadline among this agent's owned targets (a claimed-unit burst
-    // yields to it once it is within kUrgent blocks)
-    const int j_soon = any >= 0 ? owned_target(agent, any, nA) : 0x7fffffff;
+    // a claimed-unit burst yields once this owned target nears its deadline
+    const int j_soon = Jo;
     // earliest claimable unit; the cursors only grow, so a bound read at
     // the same M stays a lower bound
     int Jd = 0x7fffffff, kd = 0, cd = -1;
@@ -1266,7 +1146,6 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
     }
     const bool take_dyn = Jd < Jo;
     ACOUNT(n_sel)
-    if (!take_dyn && best < 0) best = any;  // nothing eligible or claimable: a lone pending chunk
     if (!take_dyn && best < 0) {
       // nothing to do: finished, or wait for the next source block
       bool fin = dJ < 0 && kc > P.k_max;
@@ -1375,9 +1254,9 @@ FABM_NI_AGENT __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, 
       ++tiles;
       M2 = __shfl_sync(0xffffffffu, M2, 0);
       // a newer source block: re-run the selection (owned units at once --
-      // EDF may switch to an earlier target -- unless FABM_STICKY_OWN;
-      // claimed units only when an owned target nears its deadline)
-      if (M2 != M && ((!take_dyn && !kStickyOwn) || j_soon - M2 <= kUrgent)) break;
+      // EDF may switch to an earlier target; claimed units only when an
+      // owned target nears its deadline)
+      if (M2 != M && (!take_dyn || j_soon - M2 <= kUrgent)) break;
     }
     APROF(c_tile)
     __syncwarp();
