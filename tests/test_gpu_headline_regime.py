@@ -137,3 +137,21 @@ def test_config4_members_full_N_vs_c_oracle(fabm):
         ref, _ = c_oracle.solve("financial", rhs.device_system.params, p.alpha, p.y0, grid.h, N, w,
                                 threads=c_oracle.max_threads())
         assert normwise_dev(res.states[i], ref) <= TOL, f"member {i} (alpha={p.alpha})"
+
+
+@pytest.mark.skipif(not __import__("os").environ.get("FABM_LONG_PARITY"),
+                    reason="~3 min of C oracle on 16 cores: FABM_LONG_PARITY=1 to run")
+def test_headline_N1e6_full_trajectory_vs_c_oracle(fabm):
+    """The bench workload itself -- Lorenz alpha=0.99, T=100, N=1e6, device
+    ACCURATE table -- whole trajectory against the C oracle on the same table
+    (opt-in: the oracle needs ~155 s on 16 host cores)."""
+    N, h = 1_000_000, 1e-4
+    problem = lorenz(fabm, N, h)
+    grid = fabm.GridSpec(n_steps=N, h=h)
+    traj = fabm.solve_gpu(problem, grid, weights="accurate")
+    w = device_table(problem.alpha, N)
+    ref, fref = c_oracle.solve("lorenz", problem.rhs.device_system.params, problem.alpha, problem.y0, h, N, w,
+                               threads=c_oracle.max_threads())
+    dev_s, dev_f = normwise_dev(traj.states, ref), normwise_dev(traj.f_cache, fref)
+    print(f"N=1e6 normwise deviation: states {dev_s:.3e}, f_cache {dev_f:.3e}")
+    assert dev_s <= TOL and dev_f <= TOL
