@@ -1087,6 +1087,7 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
 #ifdef FABM_PROFILE
   long long c_tile = 0, c_idle = 0, c_sw = 0, c_t = clock64();
   unsigned long long n_sel = 0, n_scan = 0, n_spill = 0, n_reload = 0, n_fin = 0, c_fin = 0, c_scan = 0, n_idle = 0;
+  unsigned long long c_top = 0, c_spl = 0;
 #define APROF(var) { const long long _t = clock64(); var += _t - c_t; c_t = _t; }
 #define ACOUNT(var) ++var;
 #else
@@ -1095,12 +1096,18 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
 #endif
   while (true) {
     int M = 0, ab = 0;
+#ifdef FABM_PROFILE
+    const long long t_top = clock64();
+#endif
     if (lane == 0) {
       M = sys ? ld_acquire_sys(&sv.ctrl->src_done) : ld_acquire_gpu(&sv.ctrl->src_done);
       ab = ld_rlx(&sv.ctrl->abort, sys);
     }
     M = __shfl_sync(0xffffffffu, M, 0);
     ab = __shfl_sync(0xffffffffu, ab, 0);
+#ifdef FABM_PROFILE
+    c_top += clock64() - t_top;
+#endif
     if (ab) return;
     if (M != last_M) {
       last_M = M;
@@ -1227,6 +1234,9 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
     // the chunk's weight window [128(J-nx)-127, 128(J-nx)+128] and f rows < 128(J-L+1) are allocated
     FABM_CHECK(P, 128LL * (J - nx) - 127 >= 0 && 128LL * (J - nx) + 128 < P.wlen &&
                       128LL * (J - kL + 1) <= P.f_rows);
+#ifdef FABM_PROFILE
+    const long long t_spl = clock64();
+#endif
     if (uid != cur_uid) {
       if (cur_uid >= 0) {
         dmma_spill_slot<D>(unit_slot<D>(P, cur_uid), lane, acc);
@@ -1241,6 +1251,9 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
       }
       cur_uid = uid;
     }
+#ifdef FABM_PROFILE
+    c_spl += clock64() - t_spl;
+#endif
     APROF(c_sw)
     // owned units: re-run the selection when a newer source block arrives;
     // claimed units: in bursts of kDynBurst chunks (fewer spill/reload
@@ -1288,7 +1301,7 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[4]), (unsigned long long)c_tile);
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[5]), (unsigned long long)c_idle);
     atomicAdd(reinterpret_cast<unsigned long long*>(&P.ctrl->prof[6]), (unsigned long long)c_sw);
-    const unsigned long long ev[8] = {n_sel, n_scan, n_spill, n_reload, n_fin, c_fin, c_scan, n_idle};
+    const unsigned long long ev[8] = {n_sel, n_scan, n_spill, c_top, n_fin, c_fin, c_scan, c_spl};
     for (int q = 0; q < 8; ++q) atomicAdd(&P.ctrl->prof2[q], ev[q]);
   }
 #endif

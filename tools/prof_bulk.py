@@ -18,9 +18,9 @@ for N in [int(x) for x in (sys.argv[1:] or ["300000", "1000000"])]:
     if hasattr(lib, "fabm_debug_prof2"):
         b2 = (ctypes.c_ulonglong * 8)()
         lib.fabm_debug_prof2(b2)
-        n_sel, n_scan, n_spill, n_reload, n_fin, c_fin, c_scan, n_idle = list(b2)
-        print(f"   per agent: selections {n_sel/agents:.0f}, cursor scans {n_scan/agents:.0f} ({c_scan/agents/cyc:.3f} of "
-              f"kernel time), spills {n_spill/agents:.0f}, reloads {n_reload/agents:.0f}, units finished "
-              f"{n_fin/agents:.0f} ({c_fin/agents/cyc:.3f} of kernel time), idle polls {n_idle/agents:.0f}; "
+        n_sel, n_scan, n_spill, c_top, n_fin, c_fin, c_scan, c_spl = list(b2)
+        print(f"   per agent: selections {n_sel/agents:.0f} (src_done acquire {c_top/agents/cyc:.3f} of kernel time), "
+              f"cursor scans {n_scan/agents:.0f} ({c_scan/agents/cyc:.3f}), spills+reloads {n_spill/agents:.0f} "
+              f"({c_spl/agents/cyc:.3f}), units finished {n_fin/agents:.0f} ({c_fin/agents/cyc:.3f}); "
               f"tiles {st['bulk_tiles']/agents:.0f}, claims {st['bulk_claims']}", flush=True)
     plan.close()
