@@ -298,40 +298,58 @@ def run_reference(args, world, rank):
     print(json.dumps(out))
 
 
-def reference_block_projection(n_target: int, prefixes=(50000, 100000)) -> dict | None:
-    """fodeabm.solve_block_parallel (unmodified, baseline/_ref) at P = all host
-    cores on two prefixes, projected to n_target."""
+def _reference_pkg():
+    """The unmodified reference package from baseline/_ref, or None."""
     ref = ROOT / "baseline" / "_ref"
     if not (ref / "fodeabm").exists():
         return None
     if str(ref) not in sys.path:
         sys.path.insert(0, str(ref))
+    import fodeabm
+
+    return fodeabm
+
+
+def _lorenz_py(t, y, sigma=10.0, rho=28.0, beta=8.0 / 3.0):
+    """The headline rhs as a plain Python callable (what a reference user passes)."""
+    return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
+
+
+def project_reference(fodeabm, solve, prefixes, n_target: int) -> dict:
+    """Time `solve(problem, grid)` of the unmodified reference on two Lorenz
+    prefixes of the headline run (same h) and project to n_target with the
+    fitted t = a*M + c*M^2 (the two-point form of the reference's
+    project_time, bench.py:160-169)."""
+    h = T_END / N_STEPS
+    samples = []
+    for m in prefixes:
+        prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=_lorenz_py, y0=Y0, t_end=m * h)
+        t0 = time.perf_counter()
+        solve(prob, fodeabm.GridSpec(n_steps=m, h=h))
+        samples.append((m, time.perf_counter() - t0))
+    (m1, t1), (m2, t2) = samples
+    c = (t2 / m2 - t1 / m1) / (m2 - m1)
+    a = max(t1 / m1 - c * m1, 0.0)
+    if c <= 0:  # per-step overheads dominate both prefixes: a quadratic through the longer one
+        c, a = t2 / (m2 * m2), 0.0
+    t_full = a * n_target + c * n_target * n_target
+    return {"projected_seconds": t_full, "prefixes": [[m1, round(t1, 4)], [m2, round(t2, 4)]],
+            "prefix_text": f"Lorenz prefixes M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s); projected "
+                           f"t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}"}
+
+
+def reference_block_projection(n_target: int, prefixes=(50000, 100000)) -> dict | None:
+    """fodeabm.solve_block_parallel (unmodified, baseline/_ref) at P = all host
+    cores on two prefixes, projected to n_target."""
     try:
-        import fodeabm
-
+        fodeabm = _reference_pkg()
+        if fodeabm is None:
+            return None
         P = os.cpu_count() or 1
-        sigma, rho, beta = 10.0, 28.0, 8.0 / 3.0
-
-        def lorenz(t, y):
-            return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
-
-        h = T_END / N_STEPS
-        samples = []
-        for m in prefixes:
-            prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
-            t0 = time.perf_counter()
-            fodeabm.solve_block_parallel(prob, fodeabm.GridSpec(n_steps=m, h=h), P)
-            samples.append((m, time.perf_counter() - t0))
-        (m1, t1), (m2, t2) = samples
-        c = (t2 / m2 - t1 / m1) / (m2 - m1)
-        a = max(t1 / m1 - c * m1, 0.0)
-        if c <= 0:
-            c, a = t2 / (m2 * m2), 0.0
-        t_full = a * n_target + c * n_target * n_target
-        return {"projected_seconds": t_full, "cores": P, "prefixes": [[m1, round(t1, 4)], [m2, round(t2, 4)]],
-                "sample": (f"fodeabm.solve_block_parallel (baseline/_ref, unmodified) P={P} workers, Lorenz prefixes "
-                           f"M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s); projected t(N)=a*N+c*N^2 = {t_full:.0f}s "
-                           f"for N={n_target}")}
+        r = project_reference(fodeabm, lambda pr, g: fodeabm.solve_block_parallel(pr, g, P), prefixes, n_target)
+        r["cores"] = P
+        r["sample"] = f"fodeabm.solve_block_parallel (baseline/_ref, unmodified) P={P} workers, {r['prefix_text']}"
+        return r
     except Exception:  # noqa: BLE001 - the C port still gives the arm a value
         return None
 
@@ -340,34 +358,14 @@ def reference_python_sample(n_target: int) -> dict | None:
     """The unmodified reference (fodeabm.solve_serial, Python + NumPy, one core)
     on two prefixes of the headline run, projected with its own O(N^2) model;
     only when the reference is installed at baseline/_ref (it travels with the
-    repo snapshot).  Reported beside the C port, which is the faster baseline."""
-    ref = ROOT / "baseline" / "_ref"
-    if not (ref / "fodeabm").exists():
-        return None
-    if str(ref) not in sys.path:
-        sys.path.insert(0, str(ref))
+    repo snapshot)."""
     try:
-        import fodeabm
-
-        sigma, rho, beta = 10.0, 28.0, 8.0 / 3.0
-
-        def lorenz(t, y):
-            return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
-
-        h = T_END / N_STEPS
-        samples = []
-        for m in (10000, 20000):
-            prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
-            t0 = time.perf_counter()
-            fodeabm.solve_serial(prob, fodeabm.GridSpec(n_steps=m, h=h))
-            samples.append((m, time.perf_counter() - t0))
-        (m1, t1), (m2, t2) = samples
-        c = (t2 / m2 - t1 / m1) / (m2 - m1)
-        a = max(t1 / m1 - c * m1, 0.0)
-        t_full = a * n_target + c * n_target * n_target
-        return {"value": n_target / t_full, "unit": UNIT, "cores": 1, "kind": "reference",
-                "sample": (f"fodeabm.solve_serial (baseline/_ref, Python+NumPy) Lorenz prefixes M={m1} ({t1:.2f}s) "
-                           f"and M={m2} ({t2:.2f}s); projected t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}")}
+        fodeabm = _reference_pkg()
+        if fodeabm is None:
+            return None
+        r = project_reference(fodeabm, fodeabm.solve_serial, (10000, 20000), n_target)
+        return {"value": n_target / r["projected_seconds"], "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"fodeabm.solve_serial (baseline/_ref, Python+NumPy) {r['prefix_text']}"}
     except Exception as exc:  # noqa: BLE001 - informational only
         return {"error": f"{type(exc).__name__}: {exc}"}
 
@@ -375,44 +373,22 @@ def reference_python_sample(n_target: int) -> dict | None:
 def reference_parallel_sample(n_target: int) -> dict | None:
     """The reference's own parallel CPU strategies (fodeabm.solve_block_parallel,
     parallel/block.py:44-236, and solve_reduction_parallel, reduction.py:139-354)
-    at P = all host cores, unmodified, on Lorenz prefixes of the headline run,
-    projected to N with t = a*N + c*N^2.  Only when the
-    reference is installed at baseline/_ref."""
-    ref = ROOT / "baseline" / "_ref"
-    if not (ref / "fodeabm").exists():
-        return None
-    if str(ref) not in sys.path:
-        sys.path.insert(0, str(ref))
+    at P = all host cores, unmodified, on Lorenz prefixes long enough for the
+    O(M^2) history term to show beside the workers' per-step synchronisation,
+    projected to N.  Only when the reference is installed."""
     out = {}
     try:
-        import fodeabm
-
+        fodeabm = _reference_pkg()
+        if fodeabm is None:
+            return None
         P = os.cpu_count() or 1
-        sigma, rho, beta = 10.0, 28.0, 8.0 / 3.0
-
-        def lorenz(t, y):
-            return (sigma * (y[1] - y[0]), y[0] * (rho - y[2]) - y[1], y[0] * y[1] - beta * y[2])
-
-        h = T_END / N_STEPS
-        for name, fn in (("block", fodeabm.solve_block_parallel), ("reduction", fodeabm.solve_reduction_parallel)):
-            samples = []
-            # prefixes long enough for the O(M^2) history term to show beside
-            # the per-step synchronisation of the workers
-            for m in (100000, 200000):
-                prob = fodeabm.FractionalProblem(alpha=ALPHA, dim=3, rhs=lorenz, y0=Y0, t_end=m * h)
-                t0 = time.perf_counter()
-                fn(prob, fodeabm.GridSpec(n_steps=m, h=h), P)
-                samples.append((m, time.perf_counter() - t0))
-            (m1, t1), (m2, t2) = samples
-            c = (t2 / m2 - t1 / m1) / (m2 - m1)
-            a = max(t1 / m1 - c * m1, 0.0)
-            if c <= 0:  # per-step overheads dominate both prefixes: a quadratic through the longer one
-                c, a = t2 / (m2 * m2), 0.0
-            t_full = a * n_target + c * n_target * n_target
-            out[name] = {"value": n_target / t_full, "unit": UNIT, "cores": P, "kind": "reference", "projected": True,
-                         "sample": (f"fodeabm.solve_{name}_parallel (baseline/_ref, unmodified) P={P} workers, "
-                                    f"Lorenz prefixes M={m1} ({t1:.2f}s) and M={m2} ({t2:.2f}s); projected "
-                                    f"t(N)=a*N+c*N^2 = {t_full:.0f}s for N={n_target}")}
+        for name, fn in (("block", lambda pr, g: fodeabm.solve_block_parallel(pr, g, P)),
+                         ("reduction", lambda pr, g: fodeabm.solve_reduction_parallel(pr, g, P))):
+            r = project_reference(fodeabm, fn, (100000, 200000), n_target)
+            out[name] = {"value": n_target / r["projected_seconds"], "unit": UNIT, "cores": P, "kind": "reference",
+                         "projected": True,
+                         "sample": f"fodeabm.solve_{name}_parallel (baseline/_ref, unmodified) P={P} workers, "
+                                   f"{r['prefix_text']}"}
     except Exception as exc:  # noqa: BLE001 - informational only
         out["error"] = f"{type(exc).__name__}: {exc}"
     return out

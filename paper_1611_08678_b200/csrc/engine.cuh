@@ -72,13 +72,13 @@ struct DevCtrl {
 
 // One shard = the bulk agents of one GPU.  Every shard holds a full copy of
 // the f history (the stepper's writer fans rows out to all copies over
-// NVLink), its own control block (src_done is released into it by the
-// stepper's publisher) and its own accumulator scratch for target switches.
-// Completed target sums go to shard 0's BK/ready.
+// NVLink) and its own control block (src_done is released into it by the
+// stepper's publisher).  The bulk units' state -- claim words, partial
+// slots, counters, cursors -- and the finished target sums (BK, ready) live
+// in shard 0's arena.
 struct ShardView {
   double* F;      // f history copy (same layout as EngineParams::F)
   DevCtrl* ctrl;  // src_done / abort polled by this shard's agents
-  double* BK;     // accumulator scratch (spills on target switches)
 };
 
 struct EngineParams {

@@ -462,7 +462,6 @@ int fabm_plan_run(fabm_plan* p, double timeout_s, fabm_status* status) {
       char* base = p->peer[sh];
       tab[sh].ctrl = reinterpret_cast<DevCtrl*>(base);
       tab[sh].F = reinterpret_cast<double*>(base + p->off_F);
-      tab[sh].BK = reinterpret_cast<double*>(base + p->off_BK);
     }
     CUDA_TRY(cudaMemcpyAsync(p->shard_tab, tab, sizeof(tab), cudaMemcpyHostToDevice, p->stream));
     P.shard = p->shard_tab;
