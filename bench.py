@@ -354,6 +354,19 @@ def reference_block_projection(n_target: int, prefixes=(50000, 100000)) -> dict 
         return None
 
 
+def reference_block_projection_clean(n_target: int) -> dict | None:
+    """reference_block_projection in a fresh interpreter: the reference forks
+    its workers, which a process holding a CUDA context (this bench arm) should
+    not do."""
+    try:
+        r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--ref-block-projection", str(n_target)],
+                           capture_output=True, text=True, timeout=600)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else None
+    except Exception:  # noqa: BLE001 - the C port still gives a baseline
+        return None
+
+
 def reference_python_sample(n_target: int) -> dict | None:
     """The unmodified reference (fodeabm.solve_serial, Python + NumPy, one core)
     on two prefixes of the headline run, projected with its own O(N^2) model;
@@ -490,7 +503,7 @@ def run_fabm(args, world, rank, local):
         # cores) or the C port, each projected from two prefixes
         info = cpu_baseline(n, args.cpu_seconds)
         cpu = {k: info[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        blk = reference_block_projection(n)
+        blk = reference_block_projection_clean(n)
         if blk is not None and n / blk["projected_seconds"] > cpu["value"]:
             cpu = {"value": n / blk["projected_seconds"], "unit": UNIT, "cores": blk["cores"], "kind": "reference",
                    "sample": blk["sample"], "c_port": cpu}
@@ -913,6 +926,9 @@ def run_csv(args, world, rank, local):
 
 
 def main():
+    if len(sys.argv) == 3 and sys.argv[1] == "--ref-block-projection":  # helper of reference_block_projection_clean
+        print(json.dumps(reference_block_projection(int(sys.argv[2]))))
+        return
     args = parse()
     world, rank, local = dist_setup(args)
     if args.workload == "batch":
