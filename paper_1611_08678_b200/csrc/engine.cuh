@@ -901,20 +901,30 @@ namespace fabm {
 constexpr int kMaxClasses = 32;
 constexpr int kDynBurst = 4;  // chunks of a claimed unit between selections (8: 200 vs 182 ms at N=1e6)
 constexpr int kUrgent = 16;  // blocks before an owned target's deadline that end a claimed-unit burst
-__device__ __forceinline__ int seg_class(int n) {
-  const int k = 31 - __clz(n) - 4;
-  return k > 0 ? k : 0;
-}
-__device__ __forceinline__ int class_lo(int k) { return k == 0 ? 1 : 1 << (k + 4); }  // n range [lo, hi)
-__device__ __forceinline__ int class_hi(int k) { return 1 << (k + 5); }
-__device__ __forceinline__ long long seg_prefix(int m, int k) {  // sum_{n'=1..m} ceil(n'/2^k)
-  const long long q = m >> k, r = m & ((1 << k) - 1);
+// segments of S = 2^k chunks, k = max(kSegMin, floor(log2 n) - 4): up to
+// 16..32 units per target, none shorter than 2^kSegMin chunks -- with one-
+// chunk units the first targets summed ~30 partials right at their deadline
+// (kSegMin 0 -> 5: N=1e5 13.2 -> 12.66 ms, N=1e6 181.2 -> 180.3 ms)
+#ifndef FABM_SEG_KMIN
+#define FABM_SEG_KMIN 5
+#endif
+constexpr int kSegMin = FABM_SEG_KMIN;
+__host__ __device__ __forceinline__ int seg_class_of_log(int lg) { return lg - 4 > kSegMin ? lg - 4 : kSegMin; }
+__device__ __forceinline__ int seg_class(int n) { return seg_class_of_log(31 - __clz(n)); }
+// class k covers n in [lo, hi): the lowest class starts at n = 1
+__host__ __device__ __forceinline__ int class_lo(int k) { return k == kSegMin ? 1 : 1 << (k + 4); }
+__host__ __device__ __forceinline__ int class_hi(int k) { return 1 << (k + 5); }
+__host__ __device__ __forceinline__ long long seg_prefix(long long m, int k) {  // sum_{n'=1..m} ceil(n'/2^k)
+  const long long q = m >> k, r = m & ((1LL << k) - 1);
   return ((q * (q + 1)) << k) / 2 + r * (q + 1);
 }
-// units of the classes below k: class 0 (n = 1..31, S = 1) has 496, class
-// j >= 1 (n = 16S..32S-1) has sum_{q=16..31} (qS + S - 1) = 392 S - 16
+// units of the classes below k: the lowest class (n = 1 .. 2^(kSegMin+5)-1)
+// has seg_prefix(2^(kSegMin+5)-1, kSegMin); class j above it (n = 16S ..
+// 32S-1, S = 2^j) has sum_{q=16..31} (qS + S - 1) = 392 S - 16
 __host__ __device__ __forceinline__ long long class_base(int k) {
-  return k == 0 ? 0 : 496 + 392 * ((1LL << k) - 2) - 16LL * (k - 1);
+  if (k <= kSegMin) return 0;
+  const long long t0 = seg_prefix((1LL << (kSegMin + 5)) - 1, kSegMin);
+  return t0 + 392 * ((1LL << k) - (2LL << kSegMin)) - 16LL * (k - 1 - kSegMin);
 }
 // unit id of (J, 0): units of targets L .. J-1
 __device__ __forceinline__ long long unit_base(const EngineParams&, int J) {
@@ -1077,7 +1087,7 @@ __device__ void bulk_agent(const EngineParams& P, BulkSmem<D>& A, int agent, int
   dmma_zero<D>(acc);
   long long cur_uid = -1;           // the unit whose chain is in acc
   int dJ = -1, ds = 0, dnext = 0;   // claimed (dynamic) unit, if any
-  int kc = 0;                       // lowest class with unclaimed columns
+  int kc = kSegMin;                 // lowest class with unclaimed columns
   int dyn_lb = 0, lb_M = -1;        // cached lower bound of the earliest claimable target (valid for lb_M)
   unsigned idle_polls = 0;
   unsigned long long tiles = 0, claims = 0;

@@ -157,17 +157,12 @@ int stride_of(int dim) { return dim == 1 ? 1 : (dim == 2 ? 2 : 4); }
 int host_seg_class(int n) {
   int lg = 0;
   while ((2 << lg) <= n) ++lg;  // floor(log2 n)
-  return std::max(0, lg - 4);
-}
-long long host_seg_prefix(long long m, int S) {
-  const long long q = m / S, r = m % S;
-  return static_cast<long long>(S) * q * (q + 1) / 2 + r * (q + 1);
+  return seg_class_of_log(lg);
 }
 long long host_unit_base(int J) {
   const int n = J - kL + 1;
-  const int k = host_seg_class(n), S = 1 << k;
-  const long long lo = k == 0 ? 1 : 1LL << (k + 4);
-  return class_base(k) + host_seg_prefix(n - 1, S) - host_seg_prefix(lo - 1, S);
+  const int k = host_seg_class(n);
+  return class_base(k) + seg_prefix(n - 1, k) - seg_prefix(class_lo(k) - 1, k);
 }
 
 }  // namespace
