@@ -259,6 +259,29 @@ struct LeaderState {
   int cA;                // chunk index of A
 };
 
+// Cold paths of the leader's waits, out of line with plain arguments (the
+// hot loop keeps only the test; its instruction footprint is what the
+// stepper's SM fetches every block).  Return the time waited in ns, or
+// kColdFailed on abort / timeout.
+constexpr unsigned long long kColdFailed = ~0ull;
+__device__ __noinline__ unsigned long long leader_wait_far_cold(const int* hflag, int m, bool live, int* sabort,
+                                                                DevCtrl* ctrl, const ShardView* shard, int n_shards,
+                                                                unsigned long long timeout_ns, int c0, int lane) {
+  const unsigned long long w0 = global_ns();
+  unsigned spins = 0;
+  while (!__all_sync(0xffffffffu, !live || ld_volatile_smem(hflag) == m)) {
+    if (((++spins) & 1023u) == 0) {
+      if (ld_volatile_smem(sabort) || *((volatile int*)&ctrl->abort)) return kColdFailed;
+      if (global_ns() - w0 > timeout_ns) {
+        if (lane == 0) raise_abort_cold(ctrl, shard, n_shards, ERR_TIMEOUT, KIND_NONE, c0, 0.0);
+        st_volatile_smem(sabort, 1);
+        return kColdFailed;
+      }
+    }
+  }
+  return global_ns() - w0;
+}
+
 // near sums of step m1 (owner lane -> all lanes via smem) and its far handoff.
 // ROT: a chunk rotation is possible at this step (the fast block path knows
 // statically where the 32-step chunk boundaries can fall).
@@ -273,20 +296,11 @@ __device__ __forceinline__ bool leader_absorb_far(const EngineParams& P, Stepper
   const int m = c0 + lane;
   const bool live = m < static_cast<int>(P.N);  // the helpers hand off steps m < N
   const int slot = m & (kHR - 1);
-  if (!__all_sync(0xffffffffu, !live || ld_volatile_smem(&S.hflag[slot]) == m)) {
-    const unsigned long long w0 = global_ns();
-    unsigned spins = 0;
-    while (!__all_sync(0xffffffffu, !live || ld_volatile_smem(&S.hflag[slot]) == m)) {
-      if (((++spins) & 1023u) == 0) {
-        if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
-        if (global_ns() - w0 > P.timeout_ns) {
-          if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, c0, 0.0);
-          st_volatile_smem(&S.abort, 1);
-          return false;
-        }
-      }
-    }
-    waited += global_ns() - w0;
+  if (__builtin_expect(!__all_sync(0xffffffffu, !live || ld_volatile_smem(&S.hflag[slot]) == m), 0)) {
+    const unsigned long long w = leader_wait_far_cold(&S.hflag[slot], m, live, &S.abort, P.ctrl, P.shard, P.n_shards,
+                                                      P.timeout_ns, c0, lane);
+    if (w == kColdFailed) return false;
+    waited += w;
   }
   __threadfence_block();  // acquire: the helpers release hflag after writing hbuf
   if (live) {
@@ -398,6 +412,26 @@ __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& 
 }
 
 
+// ring back-pressure wait (cold, out of line): until every consumer has
+// drained entry n_next+1-kRing+32
+__device__ __noinline__ unsigned long long leader_wait_ring_cold(StepperSmem* S, long long n_next, DevCtrl* ctrl,
+                                                                 const ShardView* shard, int n_shards,
+                                                                 unsigned long long timeout_ns, int lane) {
+  unsigned spins = 0;
+  const unsigned long long w0 = global_ns();
+  while (n_next - slowest_consumer(*S) > kRing - 32) {
+    if (((++spins) & 1023u) == 0) {
+      if (ld_volatile_smem(&S->abort) || *((volatile int*)&ctrl->abort)) return kColdFailed;
+      if (global_ns() - w0 > timeout_ns) {
+        if (lane == 0) raise_abort_cold(ctrl, shard, n_shards, ERR_TIMEOUT, KIND_NONE, n_next, 0.0);
+        st_volatile_smem(&S->abort, 1);
+        return kColdFailed;
+      }
+    }
+  }
+  return global_ns() - w0;
+}
+
 template <int D>
 __device__ __forceinline__ bool leader_check_block(const EngineParams& P, StepperSmem& S, const LeaderState<D>& st,
                                                    long long n_next, int lane, unsigned long long& throttled,
@@ -407,20 +441,10 @@ __device__ __forceinline__ bool leader_check_block(const EngineParams& P, Steppe
   // drained entry n+1-kRing (also keeps the mbarrier phases unaliased)
   const long long lag = n_next - slowest_consumer(S);
   lag_sum += static_cast<unsigned long long>(lag);
-  if (lag > kRing - 32) {
-    unsigned spins = 0;
-    const unsigned long long w0 = global_ns();
-    while (n_next - slowest_consumer(S) > kRing - 32) {
-      if (((++spins) & 1023u) == 0) {
-        if (ld_volatile_smem(&S.abort) || *((volatile int*)&P.ctrl->abort)) return false;
-        if (global_ns() - w0 > P.timeout_ns) {
-          if (lane == 0) raise_abort(P, ERR_TIMEOUT, KIND_NONE, n_next, 0.0);
-          st_volatile_smem(&S.abort, 1);
-          return false;
-        }
-      }
-    }
-    throttled += global_ns() - w0;
+  if (__builtin_expect(lag > kRing - 32, 0)) {
+    const unsigned long long w = leader_wait_ring_cold(&S, n_next, P.ctrl, P.shard, P.n_shards, P.timeout_ns, lane);
+    if (w == kColdFailed) return false;
+    throttled += w;
   }
   return true;
 }
@@ -511,14 +535,15 @@ __device__ void stepper_leader(const EngineParams& P, StepperSmem& S, int lane) 
   for (n = 1; n < kLeaderBlock && n < N32; ++n)
     if (!leader_step<SYS, D, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
   if (!leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
+  const int n_fast0 = n;
   while (n + kLeaderBlock <= N32) {
-    fast_blocks += kLeaderBlock / 8;
     if (!leader_run16<SYS, D, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
     n += kLeaderBlock;
     // back-pressure / abort check every 16 steps (its 9 shared-memory loads
     // stall the in-order issue); the lag bound leaves room for 16 more steps
     if (!solo && !leader_check_block<D>(P, S, st, n, lane, throttled, lag_sum)) return;
   }
+  fast_blocks = static_cast<unsigned long long>(n - n_fast0) / 8;  // (a counter in the loop costs a register)
 #pragma unroll 1
   for (; n < N32; ++n)
     if (!leader_step<SYS, D, true>(P, S, st, b0, a0, n, lane, bars_u32, waited)) return;
