@@ -952,8 +952,14 @@ namespace fabm {
 // p_{n-2} (usually long before the deadline), and whichever of {prefix,
 // final unit} arrives second adds the final unit's partial.
 constexpr int kMaxClasses = 32;
-constexpr int kDynBurst = 4;  // chunks of a claimed unit between selections (8: 200 vs 182 ms at N=1e6)
-constexpr int kUrgent = 16;  // blocks before an owned target's deadline that end a claimed-unit burst
+#ifndef FABM_DYN_BURST  // (dev overrides for A/B sweeps, tools/ab_engine.py)
+#define FABM_DYN_BURST 4
+#endif
+#ifndef FABM_URGENT
+#define FABM_URGENT 16
+#endif
+constexpr int kDynBurst = FABM_DYN_BURST;  // chunks of a claimed unit between selections (8: 200 vs 182 ms at N=1e6)
+constexpr int kUrgent = FABM_URGENT;  // blocks before an owned target's deadline that end a claimed-unit burst
 // segments of S = 2^k chunks, k = max(kSegMin, floor(log2 n) - 4): up to
 // 16..32 units per target, none shorter than 2^kSegMin chunks -- with one-
 // chunk units the first targets summed ~30 partials right at their deadline
