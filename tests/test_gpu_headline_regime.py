@@ -160,7 +160,8 @@ def test_headline_N1e6_full_trajectory_vs_c_oracle(fabm):
     assert dev_s <= TOL and dev_f <= TOL
 
 
-@pytest.mark.parametrize("system,y0,T", [("chen", (-9.0, -5.0, 14.0), 4.0), ("rossler", (0.5, 1.5, 0.1), 20.0)])
+@pytest.mark.parametrize("system,y0,T", [("chen", (-9.0, -5.0, 14.0), 4.0), ("rossler", (0.5, 1.5, 0.1), 20.0),
+                                         ("hindmarsh-rose", (0.1, 0.2, 0.2), 1000.0)])
 def test_config3_systems_multi_target_vs_c_oracle(fabm, system, y0, T):
     """Config 3's systems (Chen, Rössler; alpha = 0.9) in the multi-target
     regime: N = 2e5 on 4 bulk CTAs (64 agents owning ~25 target blocks each,
@@ -168,10 +169,12 @@ def test_config3_systems_multi_target_vs_c_oracle(fabm, system, y0, T):
     oracle on the device ACCURATE table.  Horizons: Chen's largest Lyapunov
     exponent amplifies the last-bit differences of two summation orders to
     O(1) by T = 20 (measured: 1.7 normwise), so Chen runs to T = 4 (h = 2e-5);
-    Rössler to T = 20 (h = 1e-4)."""
+    Rössler to T = 20 (h = 1e-4); Hindmarsh-Rose, the paper's Table 2
+    workload, to T = 1000 (h = 5e-3; at the paper's h = 0.01, T = 2000, the
+    two summation orders differ by 9e-13, too close to the bound)."""
     N = 200000
     h = T / N
-    rhs = {"chen": fabm.rhs_chen, "rossler": fabm.rhs_rossler}[system]()
+    rhs = {"chen": fabm.rhs_chen, "rossler": fabm.rhs_rossler, "hindmarsh-rose": fabm.rhs_hindmarsh_rose}[system]()
     problem = fabm.FractionalProblem(alpha=0.9, dim=3, rhs=rhs, y0=y0, t_end=T)
     plan = fabm.GpuPlan(problem, fabm.GridSpec(n_steps=N, h=h))
     plan.set_y0(problem.y0)
