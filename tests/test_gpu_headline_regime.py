@@ -190,3 +190,18 @@ def test_config3_systems_multi_target_vs_c_oracle(fabm, system, y0, T):
     dev_s, dev_f = normwise_dev(traj.states, ref), normwise_dev(traj.f_cache, fref)
     print(f"{system} N=2e5 T={T}: normwise deviation states {dev_s:.3e}, f_cache {dev_f:.3e}")
     assert dev_s <= TOL and dev_f <= TOL
+
+
+def test_config5_size_prefix_is_the_headline_bitwise(fabm):
+    """Size-independent property at the largest BASELINE size: the first 1e6
+    steps of the N = 1e7 config-5 trajectory (one GPU) are bitwise the
+    N = 1e6 headline solve -- the weight table, the unit partition and the
+    reduction order depend on the step / block index only, so the whole
+    N = 1e7 regime (256-chunk units, ~30 units per late target) reproduces
+    the oracle-checked headline run exactly where they overlap."""
+    h = 1e-4
+    big = fabm.solve_gpu(lorenz(fabm, 10_000_000, h), fabm.GridSpec(n_steps=10_000_000, h=h))
+    head = fabm.solve_gpu(lorenz(fabm, 1_000_000, h), fabm.GridSpec(n_steps=1_000_000, h=h))
+    assert np.array_equal(big.states[: 1_000_001], head.states)
+    assert np.array_equal(big.f_cache[: 1_000_001], head.f_cache)
+    assert np.isfinite(big.states).all()
