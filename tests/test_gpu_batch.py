@@ -112,3 +112,17 @@ def test_batch_other_systems_and_dims(fabm, kind):
         ref, fref = abm_oracle.solve_serial(p.alpha, p.y0, p.rhs, grid.h, N, weights=w)
         assert normwise_dev(res.states[i], ref) <= TOL
         assert normwise_dev(res.f_cache[i], fref) <= TOL
+
+
+def test_config4_full_sweep_members_independent_of_the_batch(fabm):
+    """BASELINE config 4 at its full size -- 4096 alphas, N = 1e5, T = 100 --
+    then four members (first, two inner, last) re-solved as a batch of
+    four: bitwise the same y_N, so every member of the full sweep is the
+    trajectory the oracle-checked small batches produce (a member's pull
+    segments and reduction order depend on its own block index only)."""
+    probs, grid = sweep(fabm, 4096, 100_000)
+    full = fabm.solve_batch_gpu(probs, grid, states=False)
+    assert full.y_last.shape == (4096, 3) and np.isfinite(full.y_last).all()
+    pick = [0, 1365, 2730, 4095]
+    few = fabm.solve_batch_gpu([probs[i] for i in pick], grid, states=False)
+    assert np.array_equal(few.y_last, full.y_last[pick])
