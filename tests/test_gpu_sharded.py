@@ -5,11 +5,13 @@ one-GPU emulation (``GpuPlan.set_virtual_shards``): every shard gets its own
 f-history copy (filled by the stepper's fan-out writes), its own control
 block (src_done released into it, abort propagated to it) and its own
 accumulator scratch, and agent CTA b serves shard (b-1) % n.  The IPC
-mapping layer between processes is the only part not exercised here; its
-host protocol is covered by tests/test_parallel_host.py (gloo, world 2).
+mapping layer between processes is exercised by tests/test_gpu_sharded_ipc.py
+(two processes on one GPU) and its host protocol by
+tests/test_parallel_host.py (gloo, world 2).
 
-Ownership of whole target blocks makes the sharded result bitwise equal to
-the single-GPU one (same tile order per target).
+The bulk units (engine.cuh "units") and the fixed-order reduction of their
+partials depend on the block index only, so the sharded result is bitwise
+equal to the single-GPU one whichever shard computed a unit.
 """
 
 from __future__ import annotations
@@ -39,7 +41,7 @@ def run_plan(fabm, prob, grid, shards):
         plan.close()
 
 
-@pytest.mark.parametrize("N", [3000, 40000, 200000])
+@pytest.mark.parametrize("N", [3000, 40000, 200000, 2000000])
 def test_virtual_shards_bitwise_equal_single(fabm, N):
     prob, grid = lorenz(fabm, N)
     ref, st1 = run_plan(fabm, prob, grid, 1)
