@@ -189,10 +189,11 @@ int fabm_plan_reset(fabm_plan* plan, fabm_status* status);
 /* ---- one trajectory sharded over the GPUs of a node (BASELINE config 5) ---
  * Replaces the reference's block-partitioned ParallelABM (parallel/block.py:
  * 44-236 with partition.py:54-74): instead of per-step partial sums from lower
- * workers, every GPU hosts bulk agents that own whole target blocks, so the
- * exchange is one NVLink store of each finished target block's sums to rank 0
- * plus the f history rows fanned out by rank 0's stepper.  Results are bitwise
- * equal to the single-GPU run.  One process per GPU: each rank creates a plan
+ * workers, every GPU hosts bulk agents that compute bulk units (fixed source
+ * segments of a target block), so the exchange is one NVLink store of each
+ * unit's partial sum into rank 0's slots -- reduced there once per target
+ * block in a fixed order -- plus the f history rows fanned out by rank 0's
+ * stepper.  Results are bitwise equal to the single-GPU run.  One process per GPU: each rank creates a plan
  * for the same problem/grid on its own device, exports its IPC handle, the
  * ranks all-gather the handles (rank order), and each calls attach. */
 #define FABM_IPC_HANDLE_BYTES 64

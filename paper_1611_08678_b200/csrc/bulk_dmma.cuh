@@ -7,10 +7,11 @@
 // diagonal shifts of one weight fragment: all 8 columns are useful for any
 // state dimension d (a (target x component) mapping would fill only d of 8).
 //
-// A bulk agent owns whole target blocks J (128 targets = two halves of 64,
-// 24 accumulator doubles per lane for d = 3, the same register budget as
-// the DFMA tile) and sweeps source chunks X = 128 I, I = 0 .. J - L, in
-// ascending order: chunk I runs sb over [X-56, X+72) in steps of 4, so column
+// A bulk agent computes one target block J at a time (128 targets = two
+// halves of 64, 24 accumulator doubles per lane for d = 3, the same register
+// budget as the DFMA tile) -- a whole block, or one unit of it (a fixed
+// segment of its sources; engine.cuh "units") -- and sweeps source chunks
+// X = 128 I in ascending order: chunk I runs sb over [X-56, X+72) in steps of 4, so column
 // j covers sources [X-56+8j, X+72+8j) -- contiguous from chunk to chunk --
 // and the last chunk adds a closing sweep sb in [X+72, X+128) whose rows past
 // the bulk end read as zero.  Every (target, source) product is taken once,

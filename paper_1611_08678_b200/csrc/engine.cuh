@@ -355,7 +355,7 @@ __device__ __forceinline__ void leader_push(LeaderState<D>& st, const PushW& w, 
 // the issue order the in-order warp needs: everything that does not depend on
 // this step's f (the gather of step n+1, its pre-sums, the push weights) is
 // issued before the chain so it completes under the chain's FP64 latencies.
-//   ROT: a chunk rotation can happen at this step (the 8-step blocks know
+//   ROT: a chunk rotation can happen at this step (the 16-step blocks know
 //        statically where the 32-step chunk boundaries can fall).
 template <int SYS, int D, bool ROT, int ARRIVE = 1>
 __device__ __forceinline__ bool leader_step(const EngineParams& P, StepperSmem& S, LeaderState<D>& st,
