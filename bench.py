@@ -904,7 +904,7 @@ def run_csv(args, world, rank, local):
     peak = peaks.get("hbm_gbs", 7700.0)
     achieved = alg / (step_ms * 1e-3) / 1e9
     print(json.dumps({
-        "metric": "trajectory CSV rows/sec (write_trajectory_csv of the Lorenz N=1e6 solve)",
+        "metric": f"trajectory CSV rows/sec (write_trajectory_csv of the Lorenz N={n:.0e} solve)",
         "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u8", "data": "synthetic (the headline Lorenz trajectory)",
